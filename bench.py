@@ -1,0 +1,405 @@
+"""bench.py — QSVM kernel entries/s at 784 qubits (BASELINE.json metric) on 1..8 B200.
+
+Workload (BASELINE.json configs[3], the config the 1/2/4/8-GPU metric is quoted on; it fits one
+GPU): MNIST-shaped synthetic data, 784 qubits, L = 2, train Gram 10000 x 10000 (49,995,000
+strict-upper entries; diagonal injected) + test-versus-train cross 2000 x 10000 (20,000,000
+entries).  One step = gate build + pair sweeps + (N > 1) NCCL gather + unpack of the whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+value       whole-job entries/s, device-resident inputs, CUDA events, max over ranks
+e2e         same metric through the public API with host (pinned) buffers, H2D + D2H inside
+roofline    sweep kernel, executed FP64 flops / CUDA-event launch time vs B200 FP64 peak
+cpu_baseline  oracle/ (the reference's contraction restated in C) on the host cores, sampled
+--impl reference  that CPU baseline as the reference arm (rank 0 only)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "QSVM kernel entries/sec at 784 qubits, 1/2/4/8 B200; % of FP64 roofline"
+UNIT = "entries/s"
+N_QUBITS, N_TRAIN, N_TEST, LAYERS = 784, 10000, 2000, 2
+WORKLOAD = {"workload": "configs[3]: MNIST-shaped synthetic, 10-class, 784 qubits, "
+                        "10000 train Gram (strict upper) + 2000x10000 test-vs-train cross",
+            "qubits": N_QUBITS, "layers": LAYERS, "n_train": N_TRAIN, "n_test": N_TEST,
+            "convention": "probability", "angle_bandwidth": 1.0,
+            "l2": "inputs larger than L2: 150 MB gate planes + 960 MB kernel output per step"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload_data():
+    from paper_2405_02630_b200.data import config_data
+
+    Atr, ytr, Ate, yte = config_data(4, N_TRAIN, N_TEST, "mnist", bw=1.0)
+    return Atr, Ate
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline (the oracle: the reference's TN contraction restated in C, all host threads)
+# ------------------------------------------------------------------------------------------
+def cpu_baseline_run(Atr, Ate, seconds: float, seed: int = 0):
+    from oracle import oracle
+
+    threads = host_threads()
+    rng = np.random.default_rng(seed)
+    n_gram = N_TRAIN * (N_TRAIN - 1) // 2
+    total = n_gram + N_TEST * N_TRAIN
+    A = np.concatenate([Atr, Ate])
+
+    def sample(P):
+        # uniform over the job's pair set: Gram strict-upper pairs + cross pairs
+        out = np.empty((P, 2), dtype=np.int64)
+        for k in range(P):
+            while True:
+                if rng.integers(total) < n_gram:
+                    i, j = rng.integers(N_TRAIN, size=2)
+                    if i < j:
+                        out[k] = (i, j)
+                        break
+                else:
+                    out[k] = (N_TRAIN + rng.integers(N_TEST), rng.integers(N_TRAIN))
+                    break
+        return out
+
+    cal = sample(max(threads * 2, 8))
+    t0 = time.perf_counter()
+    oracle.amplitudes(A, A, cal, LAYERS, threads)
+    rate = len(cal) / (time.perf_counter() - t0)
+    P = int(max(threads * 4, min(rate * seconds, 2_000_000)))
+    pairs = sample(P)
+    t0 = time.perf_counter()
+    oracle.amplitudes(A, A, pairs, LAYERS, threads)
+    dt = time.perf_counter() - t0
+    return {"value": P / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{P} pairs sampled uniformly from the workload's 69,995,000 "
+                      f"(seed {seed}); oracle/qk_oracle.c complex128 TN contraction, "
+                      f"{threads} pthreads on {cpu_model()}",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    Atr, Ate = workload_data()
+    per_step = max(2.0, min(8.0, 120.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline_run(Atr, Ate, per_step, seed=s)
+        if s >= args.warmup:
+            vals.append(r)
+    v = float(np.median([r["value"] for r in vals]))
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median([r["seconds"] for r in vals])),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+           "config": dict(WORKLOAD),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
+                            "sample": vals[0]["sample"]},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "reference = oracle/ port of the reference's tensor-network contraction "
+                   "(the reference is pure Python; /root/reference is absent on the GPU box); "
+                   "each step times a bounded pair sample of the same workload"}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/qk_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines()[1:]:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1].split()[0]))
+                smax.append(float(f[2].split()[0]))
+                power.append(float(f[3].split()[0]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s, p in zip(sm, power) if p > 0.5 * max(power)] if power else sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2405_02630_b200 import (FeatureMapConfig, compute_cross_kernel,
+                                       compute_kernel_matrix, plan_for)
+    from paper_2405_02630_b200 import device as qdev
+    from paper_2405_02630_b200.distributed import KernelJob
+
+    cfg = FeatureMapConfig(N_QUBITS, layers=LAYERS)
+    plan = plan_for(cfg)
+    info = plan.info
+    Atr, Ate = workload_data()
+    tr = torch.as_tensor(Atr, device="cuda")
+    te = torch.as_tensor(Ate, device="cuda")
+    job = KernelJob(plan, N_TRAIN, N_TEST)
+    entries = job.layout.entries()
+
+    # Instrument the sweep launches with CUDA events on the launching (current) stream.
+    sweep_events = []
+    orig_gram, orig_cross = qdev.gram, qdev.cross
+
+    def timed(fn):
+        def wrap(*a, **k):
+            s = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            out = fn(*a, **k)
+            e1.record(s)
+            if recording[0]:
+                sweep_events.append((e0, e1))
+            return out
+        return wrap
+
+    recording = [False]
+    qdev.gram, qdev.cross = timed(orig_gram), timed(orig_cross)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        job.run(tr, te)
+    barrier()
+    clocks = Clocks(local)
+    if rank == 0:
+        clocks.start()
+    barrier()
+    recording[0] = True
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        job.run(tr, te)
+    t1.record()
+    torch.cuda.synchronize()
+    recording[0] = False
+    elapsed = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    barrier()
+    clk = clocks.stop() if rank == 0 else None
+    qdev.gram, qdev.cross = orig_gram, orig_cross
+
+    sweep_s = sum(a.elapsed_time(b) for a, b in sweep_events) / 1e3
+    launches_per_step = 2 + len(sweep_events) // max(1, args.steps)
+    if world > 1 and rank == 0:
+        launches_per_step += sum(len(job.layout.segments(r)) for r in range(world))
+    value = entries * args.steps / elapsed
+
+    # roofline of the dominant kernel (the pair sweep), per rank, from live CUDA events
+    n_sweep = len(sweep_events)
+    my_entries = entries / world
+    flops_exec = my_entries * info["flops_per_entry"] * args.steps
+    achieved_tf = flops_exec / sweep_s / 1e12 if sweep_s > 0 else None
+    props = torch.cuda.get_device_properties(local)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_nominal = props.multi_processor_count * 128 * sm_max * 1e6 / 1e12
+    peak_dfma = qdev.dfma_peak_flops() / 1e12
+    traffic = None
+    try:
+        tj = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        traffic = tj.get("sweep_dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_nominal,
+                "unit": "TFLOP/s", "frac": (achieved_tf / peak_nominal) if achieved_tf else None,
+                "traffic": traffic, "kernel": "qk::sweep_kernel<2,*,0>",
+                "flops_per_entry_executed": info["flops_per_entry"],
+                "flops_per_entry_algorithmic_F": info["algorithmic_flops_per_entry"],
+                "dp_instr_per_entry": info["dp_instr_per_entry"],
+                "fp64_pipe_frac": (my_entries * args.steps * info["dp_instr_per_entry"] /
+                                   sweep_s / (props.multi_processor_count * 64 * sm_max * 1e6))
+                if sweep_s > 0 else None,
+                "peak_measured_dfma": peak_dfma,
+                "peak_note": "nominal FP64 = SMs x 64 DFMA/clk x 2 x sm_max_mhz (FP64 is not in "
+                             "MEASURED_PEAKS.json); peak_measured_dfma = qk_dfma_peak "
+                             "microbenchmark in this run",
+                "sweep_share_of_step": sweep_s / elapsed if elapsed > 0 else None,
+                "sweep_launches": n_sweep}
+
+    # e2e through the public API with pinned host buffers (N = 1: the C-ABI host pipeline;
+    # N > 1: per-rank H2D + sharded job + gather + D2H on rank 0)
+    e2e = None
+    if args.e2e_steps > 0:
+        h_tr = torch.empty(Atr.shape, dtype=torch.float64, pin_memory=True).numpy()
+        h_te = torch.empty(Ate.shape, dtype=torch.float64, pin_memory=True).numpy()
+        h_tr[:] = Atr
+        h_te[:] = Ate
+        h2d = h_tr.nbytes + h_te.nbytes
+        d2h = 8 * (N_TRAIN * N_TRAIN + N_TEST * N_TRAIN)
+        if world == 1:
+            h_K = torch.empty((N_TRAIN, N_TRAIN), dtype=torch.float64, pin_memory=True).numpy()
+            h_Kx = torch.empty((N_TEST, N_TRAIN), dtype=torch.float64, pin_memory=True).numpy()
+            h2d += h_tr.nbytes  # the cross call uploads the train angles again
+
+            def e2e_step():
+                compute_kernel_matrix(h_tr, cfg, out=h_K)
+                compute_cross_kernel(h_te, h_tr, cfg, out=h_Kx)
+        else:
+            h_K = torch.empty((N_TRAIN, N_TRAIN), dtype=torch.float64,
+                              pin_memory=True) if rank == 0 else None
+            h_Kx = torch.empty((N_TEST, N_TRAIN), dtype=torch.float64,
+                               pin_memory=True) if rank == 0 else None
+            t_tr = torch.from_numpy(h_tr)
+            t_te = torch.from_numpy(h_te)
+
+            def e2e_step():
+                Ktr, Kx = job.run(t_tr.to("cuda", non_blocking=True),
+                                  t_te.to("cuda", non_blocking=True))
+                if rank == 0:
+                    h_K.copy_(Ktr, non_blocking=True)
+                    h_Kx.copy_(Kx, non_blocking=True)
+                torch.cuda.synchronize()
+        e2e_step()
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        e_el = time.perf_counter() - w0
+        if world > 1:
+            tt = torch.tensor([e_el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_el = float(tt.item())
+        e2e = {"value": entries * args.e2e_steps / e_el, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d * (world if world > 1 else 1)),
+               "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
+               "ms_per_step": 1e3 * e_el / args.e2e_steps,
+               "api": "compute_kernel_matrix + compute_cross_kernel (C-ABI host pipeline)"
+               if world == 1 else "KernelJob over NCCL + pinned H2D/D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_run(Atr, Ate, args.cpu_seconds)
+        cpu.pop("seconds", None)
+
+    launches_total = torch.tensor([launches_per_step * args.steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(launches_total)
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": dict(WORKLOAD, parallelism=f"tile-sharded x{world}",
+                              entries_per_step=entries),
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+               "gpu_launches": int(launches_total.item()),
+               "gpu": props.name, "plan": info}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,116 @@
+"""ctypes binding of libqk.so — the C ABI declared in include/qk.h.
+
+The library is the only compute path of this package.  If it is missing or fails to load,
+every entry point raises :class:`NativeLibraryError`; nothing falls back to the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+from .errors import CapacityError, DeviceError, NativeLibraryError, RebindError, StructuralError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libqk.so"
+HEADER = Path(__file__).resolve().parent.parent / "include" / "qk.h"
+
+QK_OK, QK_ERR_VALUE, QK_ERR_REBIND, QK_ERR_CAPACITY, QK_ERR_STRUCTURAL, QK_ERR_CUDA = range(6)
+QK_PROBABILITY, QK_MAGNITUDE = 0, 1
+QK_OUT_DENSE, QK_OUT_PACKED = 0, 1
+
+_c_i32, _c_i64, _c_vp, _c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int32), ("layers", ctypes.c_int32), ("convention", ctypes.c_int32),
+        ("bond", ctypes.c_int32), ("tile_edge", ctypes.c_int32), ("chunk", ctypes.c_int32),
+        ("width_padded", ctypes.c_int32), ("stages", ctypes.c_int32),
+        ("dp_instr_per_entry", ctypes.c_int64), ("flops_per_entry", ctypes.c_int64),
+        ("algorithmic_flops_per_entry", ctypes.c_int64),
+        ("reference_cmacs_per_entry", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+_SIGNATURES = {
+    "qk_abi_version": (ctypes.c_int, []),
+    "qk_last_error": (ctypes.c_char_p, []),
+    "qk_plan_create": (ctypes.c_int, [_c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_vp)]),
+    "qk_plan_destroy": (ctypes.c_int, [_c_vp]),
+    "qk_plan_get_info": (ctypes.c_int, [_c_vp, ctypes.POINTER(PlanInfo)]),
+    "qk_planes_bytes": (_c_sz, [_c_vp, _c_i64]),
+    "qk_gram_tile_count": (_c_i64, [_c_vp, _c_i64]),
+    "qk_cross_tile_count": (_c_i64, [_c_vp, _c_i64, _c_i64]),
+    "qk_gate_build": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "qk_gram_tiles": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_i32, _c_vp]),
+    "qk_unpack_gram": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "qk_cross_tiles": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp,
+                                      _c_i64, _c_i32, _c_vp]),
+    "qk_unpack_cross": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
+                                       _c_i64, _c_vp]),
+    "qk_pair_amplitudes": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_i64,
+                                          _c_vp, _c_vp]),
+    "qk_kernel_matrix_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp]),
+    "qk_cross_kernel_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp]),
+    "qk_dfma_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), _c_vp]),
+}
+
+_lib = None
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/qk.h (the ABI contract)."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\*]+\s*\**\s*(qk_\w+)\s*\(", text, re.M)))
+
+
+def lib() -> ctypes.CDLL:
+    """Load libqk.so once; raise NativeLibraryError if it is absent or incomplete."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeLibraryError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc, sm_100a); there is no CPU fallback")
+    try:
+        handle = ctypes.CDLL(str(LIB_PATH))
+    except OSError as exc:
+        raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, (restype, argtypes) in _SIGNATURES.items():
+        try:
+            fn = getattr(handle, name)
+        except AttributeError as exc:
+            raise NativeLibraryError(f"{LIB_PATH} does not export {name}") from exc
+        fn.restype = restype
+        fn.argtypes = argtypes
+    if handle.qk_abi_version() != 1:
+        raise NativeLibraryError("libqk ABI version mismatch")
+    _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().qk_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, context: str | None = None) -> None:
+    """Map a qk_status onto the reference's exception hierarchy (errors.py:8-47)."""
+    if status == QK_OK:
+        return
+    msg = last_error()
+    if context:
+        msg = f"{context}: {msg}"
+    if status == QK_ERR_VALUE:
+        raise ValueError(msg)
+    if status == QK_ERR_REBIND:
+        raise RebindError(msg)
+    if status == QK_ERR_CAPACITY:
+        raise CapacityError(msg)
+    if status == QK_ERR_STRUCTURAL:
+        raise StructuralError(msg)
+    raise DeviceError(msg)

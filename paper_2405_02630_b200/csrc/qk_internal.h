@@ -1,0 +1,51 @@
+// qk_internal.h — shared host-side definitions of libqk (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "qk.h"
+
+namespace qk {
+
+// Sweep geometry shared by the planner, the gate-build kernel and the sweep kernels.
+constexpr int kTile = 64;    // samples per plane block == tile edge T
+constexpr int kChunk = 16;   // qubits per bulk-copy chunk Q
+constexpr int kStages = 4;   // shared-memory ring depth
+constexpr int kRescaleChunks = 32;  // L=2: multiply the bond state by 2^-512 every 512 qubits
+
+struct Plan {
+  int32_t width = 0;
+  int32_t layers = 0;
+  int32_t convention = 0;
+  int32_t width_padded = 0;  // multiple of kChunk; the first (width_padded - width) rows are identity
+  int32_t front_pad = 0;
+  double final_scale = 1.0;  // 2^-(width_padded - 512 * rescales) for L = 2, 1 for L = 1
+  qk_plan_info info{};
+};
+
+qk_status set_error(qk_status code, const std::string& msg);
+qk_status check_plan(const qk_plan* p, const Plan** out);
+
+int64_t blocks_for(int64_t n_samples);
+
+// Device launchers (qk_sweep.cu).  They return QK_OK or a QK_ERR_CUDA status.
+qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
+                            void* d_planes, uint64_t* d_bad, void* stream);
+qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
+                       const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
+                       double* d_out, int64_t ld_out, int out_mode, void* stream);
+qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
+                        int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
+                        int64_t ld, void* stream);
+qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* d_b, int64_t n_b,
+                       const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream);
+qk_status launch_dfma_peak(double* out, void* stream);
+
+enum SweepMode { kModeGram = 0, kModeCross = 1 };
+
+}  // namespace qk
+
+struct qk_plan {
+  qk::Plan p;
+};

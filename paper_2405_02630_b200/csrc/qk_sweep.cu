@@ -1,0 +1,580 @@
+// qk_sweep.cu — sm_100a kernels of the QSVM quantum-kernel hot path.
+//
+//   gate_build_kernel : angles [N x n] -> per-(sample, qubit) rotation planes (HBM-bound)
+//   sweep_kernel      : pair-tiled overlap contraction, bond state in registers (FP64-bound)
+//   pairs_kernel      : same recurrence for an explicit pair list (contract_batch drop-in)
+//   unpack_kernel     : packed tiles -> dense (symmetrised) kernel matrix
+//   dfma_peak_kernel  : FP64 FMA issue-rate microbenchmark (roofline denominator check)
+//
+// The math (derivation in DESIGN.md §2).  For L = 2 the kernel circuit of a pair
+// (circuit.py:151-157) is  U(x_i)^dag U(x_j) = R(-x_i) C^dag R(x_j - x_i) C R(x_j)  after the
+// middle C C^dag cancels, so the amplitude is the overlap of two bond-2 MPS and reduces to a
+// bond-4 transfer sweep along the qubit chain.  In the rotated basis
+//     S+ = V00 + V11,  T+ = V01 + V10,  S- = V00 - V11,  T- = V01 - V10
+// with full-angle per-sample values a = cos x, b = sin x and C = cos(x_j - x_i),
+// D = sin(x_j - x_i), one qubit is (the 1/2 per qubit is folded into one exact power-of-two
+// scale at the end):
+//     S+' = (1 + C) S+ + (b_i + b_j) T+        T-' = (a_j - a_i) S+ - D T+
+//     S-' = (a_i + a_j) S- + D T-              T+' = (b_i - b_j) T- - (1 - C) S-
+// amp = (S+ + T+) 2^-n.  That is 16 FP64 instructions per pair-qubit (2 DMUL, 4 DADD,
+// 10 DFMA) against 24 for the textbook (A_i^T V A_j) o RY(delta) form.
+// For L = 1 the amplitude is prod_q cos((x_j - x_i)/2) from half-angle planes.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "qk_internal.h"
+
+namespace qk {
+
+constexpr int kThreads = 256;
+constexpr int kTX = 16;                 // threads along j
+constexpr int kTY = kThreads / kTX;     // threads along i
+constexpr int kRI = kTile / kTY;        // i-samples per thread (4)
+constexpr int kRJ = kTile / kTX;        // j-samples per thread (4)
+constexpr int kChunkElems = kChunk * kTile;            // double2 per block-chunk
+constexpr uint32_t kChunkBytes = kChunkElems * 16;     // 16 KB
+constexpr size_t kSmemBytes = size_t(kStages) * 2 * kChunkBytes + kStages * 8;
+
+static_assert(kRI * kTY == kTile && kRJ * kTX == kTile, "tile mapping");
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers: mbarrier + bulk async copy (TMA engine, SASS UBLKCP)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "QK_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra QK_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// The per-qubit recurrences (shared by the tile sweep and the pair-list kernel so the two
+// produce bit-identical amplitudes).
+// ------------------------------------------------------------------------------------------
+struct Bond4 {
+  double sp, tp, sm, tm;
+};
+
+__device__ __forceinline__ void bond4_init(Bond4& s) {
+  s.sp = 1.0;
+  s.tp = 0.0;
+  s.sm = 1.0;
+  s.tm = 0.0;
+}
+
+__device__ __forceinline__ void bond4_step(Bond4& s, double2 vi, double2 vj) {
+  const double ai = vi.x, bi = vi.y, aj = vj.x, bj = vj.y;
+  const double c = fma(bi, bj, ai * aj);   // cos(x_j - x_i)
+  const double d = fma(ai, bj, -(bi * aj));  // sin(x_j - x_i)
+  const double s1 = bi + bj, d2 = bi - bj, s2 = ai + aj, d1 = aj - ai;
+  const double nsp = fma(s1, s.tp, fma(c, s.sp, s.sp));
+  const double ntm = fma(d1, s.sp, -(d * s.tp));
+  const double nsm = fma(d, s.tm, s2 * s.sm);
+  const double ntp = fma(d2, s.tm, fma(c, s.sm, -s.sm));
+  s.sp = nsp;
+  s.tp = ntp;
+  s.sm = nsm;
+  s.tm = ntm;
+}
+
+__device__ __forceinline__ void bond4_scale(Bond4& s, double f) {
+  s.sp *= f;
+  s.tp *= f;
+  s.sm *= f;
+  s.tm *= f;
+}
+
+__device__ __forceinline__ double bond4_amp(const Bond4& s, double final_scale) {
+  return (s.sp + s.tp) * final_scale;
+}
+
+struct Bond1 {
+  double v;
+};
+__device__ __forceinline__ void bond1_init(Bond1& s) { s.v = 1.0; }
+__device__ __forceinline__ void bond1_step(Bond1& s, double2 vi, double2 vj) {
+  s.v *= fma(vi.y, vj.y, vi.x * vj.x);  // cos((x_j - x_i)/2) from half-angle planes
+}
+
+template <int LAYERS>
+struct BondT;
+template <>
+struct BondT<1> {
+  using type = Bond1;
+};
+template <>
+struct BondT<2> {
+  using type = Bond4;
+};
+
+template <int LAYERS>
+__device__ __forceinline__ void st_init(typename BondT<LAYERS>::type& s) {
+  if constexpr (LAYERS == 2) bond4_init(s); else bond1_init(s);
+}
+template <int LAYERS>
+__device__ __forceinline__ void st_step(typename BondT<LAYERS>::type& s, double2 vi, double2 vj) {
+  if constexpr (LAYERS == 2) bond4_step(s, vi, vj); else bond1_step(s, vi, vj);
+}
+template <int LAYERS>
+__device__ __forceinline__ void st_rescale(typename BondT<LAYERS>::type& s) {
+  if constexpr (LAYERS == 2) bond4_scale(s, 0x1p-512);
+}
+template <int LAYERS>
+__device__ __forceinline__ double st_amp(const typename BondT<LAYERS>::type& s, double fs) {
+  if constexpr (LAYERS == 2) return bond4_amp(s, fs); else return s.v;
+}
+
+__device__ __forceinline__ double kernel_value(double amp, int convention) {
+  return convention == QK_MAGNITUDE ? fabs(amp) : amp * amp;
+}
+
+// Upper-triangle tile list, row-major over nb plane blocks: row b holds tiles (b, b..nb-1).
+__device__ __forceinline__ void decode_upper(int64_t g, int64_t nb, int64_t& bi, int64_t& bj) {
+  const double m = 2.0 * double(nb) + 1.0;
+  int64_t b = int64_t((m - sqrt(m * m - 8.0 * double(g))) * 0.5);
+  if (b < 0) b = 0;
+  if (b > nb - 1) b = nb - 1;
+  auto off = [nb](int64_t r) { return r * nb - r * (r - 1) / 2; };
+  while (b > 0 && off(b) > g) --b;
+  while (b + 1 < nb && off(b + 1) <= g) ++b;
+  bi = b;
+  bj = b + (g - off(b));
+}
+
+// ------------------------------------------------------------------------------------------
+// Gate build: angles -> planes[block][q][t] = (cos x, sin x)  (L = 2)  or  half angles (L = 1)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gate_build_kernel(const double* __restrict__ X,
+                                                         int64_t n_samples, int64_t ld,
+                                                         int width, int n_pad, int front,
+                                                         int half, double2* __restrict__ planes,
+                                                         unsigned long long* bad) {
+  __shared__ double tile[kTile][33];
+  const int64_t blk = blockIdx.x;
+  const int q0 = blockIdx.y * 32;
+  for (int idx = threadIdx.x; idx < kTile * 32; idx += blockDim.x) {
+    const int t = idx >> 5, qq = idx & 31;
+    const int64_t s = blk * kTile + t;
+    const int q = q0 + qq - front;
+    double x = 0.0;
+    if (s < n_samples && q >= 0 && q < width) {
+      x = __ldg(X + s * ld + q);
+      if (bad != nullptr && !isfinite(x)) atomicMin(bad, (unsigned long long)s);
+    }
+    tile[t][qq] = x;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kTile * 32; idx += blockDim.x) {
+    const int qq = idx >> 6, t = idx & 63;
+    const int q = q0 + qq;
+    if (q >= n_pad) break;
+    const double x = tile[t][qq];
+    double sn, cs;
+    sincos(half ? 0.5 * x : x, &sn, &cs);
+    planes[(blk * n_pad + q) * kTile + t] = make_double2(cs, sn);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Pair-tiled sweep.  Persistent CTAs walk tiles g = tile_begin + blockIdx.x + k*gridDim.x;
+// the (tile, chunk) stream is fed by one thread through a kStages-deep ring of bulk copies
+// (i-block chunk + j-block chunk, 32 KB per stage) completing on an mbarrier.  Each thread
+// owns a kRI x kRJ micro-tile of pairs whose bond states live in registers for the whole
+// qubit sweep; per qubit it reads kRI + kRJ double2 from shared memory (broadcast within
+// the warp) and issues 16 * kRI * kRJ FP64 instructions.
+// ------------------------------------------------------------------------------------------
+struct SweepArgs {
+  const double2* rows;
+  const double2* cols;
+  int64_t n_rows, n_cols;
+  int64_t nb_rows, nb_cols;
+  int64_t tile_begin, n_tiles;
+  double* out;
+  int64_t ld_out;
+  double final_scale;
+  int n_pad, nchunks, convention;
+};
+
+template <int LAYERS, int MODE, int OUT>
+__global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepArgs a) {
+  using St = typename BondT<LAYERS>::type;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sbuf = reinterpret_cast<double2*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(kStages) * 2 * kChunkBytes);
+
+  const int tid = threadIdx.x;
+  const int tx = tid % kTX, ty = tid / kTX;
+  const int64_t my_tiles =
+      a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nchunks = a.nchunks;
+  const int64_t F = my_tiles * nchunks;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto tile_of = [&](int64_t k, int64_t& bi, int64_t& bj) {
+    const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
+    if (MODE == kModeGram) {
+      decode_upper(g, a.nb_rows, bi, bj);
+    } else {
+      bi = g / a.nb_cols;
+      bj = g - bi * a.nb_cols;
+    }
+  };
+  auto issue = [&](int64_t f) {
+    const int64_t k = f / nchunks;
+    const int c = int(f - k * nchunks);
+    int64_t bi, bj;
+    tile_of(k, bi, bj);
+    const int stage = int(f % kStages);
+    double2* dst = sbuf + size_t(stage) * 2 * kChunkElems;
+    const double2* si = a.rows + (bi * a.n_pad + int64_t(c) * kChunk) * kTile;
+    const double2* sj = a.cols + (bj * a.n_pad + int64_t(c) * kChunk) * kTile;
+    mbar_arrive_expect_tx(&full[stage], 2 * kChunkBytes);
+    bulk_g2s(dst, si, kChunkBytes, &full[stage]);
+    bulk_g2s(dst + kChunkElems, sj, kChunkBytes, &full[stage]);
+  };
+
+  if (tid == 0) {
+    const int64_t pre = F < kStages - 1 ? F : kStages - 1;
+    for (int64_t f = 0; f < pre; ++f) issue(f);
+  }
+
+  St st[kRI][kRJ];
+  int64_t f = 0;
+  for (int64_t k = 0; k < my_tiles; ++k) {
+#pragma unroll
+    for (int r = 0; r < kRI; ++r)
+#pragma unroll
+      for (int c = 0; c < kRJ; ++c) st_init<LAYERS>(st[r][c]);
+
+    for (int ch = 0; ch < nchunks; ++ch, ++f) {
+      if (tid == 0 && f + kStages - 1 < F) issue(f + kStages - 1);
+      const int stage = int(f % kStages);
+      mbar_wait(&full[stage], uint32_t((f / kStages) & 1));
+      const double2* sI = sbuf + size_t(stage) * 2 * kChunkElems;
+      const double2* sJ = sI + kChunkElems;
+#pragma unroll 4
+      for (int q = 0; q < kChunk; ++q) {
+        double2 vi[kRI], vj[kRJ];
+#pragma unroll
+        for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty + kTY * r];
+#pragma unroll
+        for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
+#pragma unroll
+        for (int r = 0; r < kRI; ++r)
+#pragma unroll
+          for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+      }
+      if (LAYERS == 2 && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0) {
+#pragma unroll
+        for (int r = 0; r < kRI; ++r)
+#pragma unroll
+          for (int c = 0; c < kRJ; ++c) st_rescale<LAYERS>(st[r][c]);
+      }
+      __syncthreads();  // every thread is done with this stage before it is refilled
+    }
+
+    // ---- epilogue ----
+    int64_t bi, bj;
+    tile_of(k, bi, bj);
+    if (OUT == QK_OUT_PACKED) {
+      const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
+      double* o = a.out + (g - a.tile_begin) * int64_t(kTile * kTile);
+#pragma unroll
+      for (int r = 0; r < kRI; ++r)
+#pragma unroll
+        for (int c = 0; c < kRJ; ++c)
+          o[(ty + kTY * r) * kTile + tx + kTX * c] =
+              kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRI; ++r) {
+        const int64_t i = bi * kTile + ty + kTY * r;
+#pragma unroll
+        for (int c = 0; c < kRJ; ++c) {
+          const int64_t j = bj * kTile + tx + kTX * c;
+          const double v = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
+          if (MODE == kModeGram) {
+            if (i < a.n_rows && j < a.n_rows) {
+              if (i < j) {
+                a.out[i * a.ld_out + j] = v;
+                a.out[j * a.ld_out + i] = v;
+              } else if (i == j) {
+                a.out[i * a.ld_out + i] = 1.0;
+              }
+            }
+          } else {
+            if (i < a.n_rows && j < a.n_cols) a.out[i * a.ld_out + j] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Pair-list kernel: one pair per thread, planes read straight from global/L2.
+// ------------------------------------------------------------------------------------------
+template <int LAYERS>
+__global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ A, int64_t n_a,
+                                                    const double2* __restrict__ B, int64_t n_b,
+                                                    const int64_t* __restrict__ pairs,
+                                                    int64_t n_pairs, double* __restrict__ amp,
+                                                    int n_pad, int nchunks, double final_scale) {
+  using St = typename BondT<LAYERS>::type;
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n_pairs) return;
+  const int64_t p = pairs[2 * k], q = pairs[2 * k + 1];
+  if (p < 0 || p >= n_a || q < 0 || q >= n_b) {
+    amp[k] = __longlong_as_double(0x7ff8000000000000LL);
+    return;
+  }
+  const double2* a = A + (p / kTile) * int64_t(n_pad) * kTile + (p % kTile);
+  const double2* b = B + (q / kTile) * int64_t(n_pad) * kTile + (q % kTile);
+  St s;
+  st_init<LAYERS>(s);
+  for (int ch = 0; ch < nchunks; ++ch) {
+#pragma unroll 4
+    for (int qq = 0; qq < kChunk; ++qq) {
+      const int64_t off = int64_t(ch * kChunk + qq) * kTile;
+      st_step<LAYERS>(s, __ldg(a + off), __ldg(b + off));
+    }
+    if (LAYERS == 2 && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0) st_rescale<LAYERS>(s);
+  }
+  amp[k] = st_amp<LAYERS>(s, final_scale);
+}
+
+// ------------------------------------------------------------------------------------------
+// Unpack packed tiles (multi-rank gather output) into the dense kernel matrix.
+// ------------------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(256) unpack_kernel(const double* __restrict__ packed,
+                                                     int64_t n_rows, int64_t n_cols,
+                                                     int64_t nb_rows, int64_t nb_cols,
+                                                     int64_t tile_begin, double* __restrict__ K,
+                                                     int64_t ld) {
+  const int64_t g = tile_begin + blockIdx.x;
+  int64_t bi, bj;
+  if (MODE == kModeGram) {
+    decode_upper(g, nb_rows, bi, bj);
+  } else {
+    bi = g / nb_cols;
+    bj = g - bi * nb_cols;
+  }
+  const double* src = packed + int64_t(blockIdx.x) * kTile * kTile;
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int il = e / kTile, jl = e % kTile;
+    const int64_t i = bi * kTile + il, j = bj * kTile + jl;
+    const double v = src[e];
+    if (MODE == kModeGram) {
+      if (i < n_rows && j < n_rows) {
+        if (i < j) {
+          K[i * ld + j] = v;
+          K[j * ld + i] = v;
+        } else if (i == j) {
+          K[i * ld + i] = 1.0;
+        }
+      }
+    } else if (i < n_rows && j < n_cols) {
+      K[i * ld + j] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// FP64 FMA issue-rate microbenchmark: 8 independent DFMA chains per thread.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  const double m = 0.999999999, c = 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(x[k], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.0) out[0] = s;  // keep the chains alive
+}
+
+// ------------------------------------------------------------------------------------------
+// Launchers
+// ------------------------------------------------------------------------------------------
+static qk_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return QK_OK;
+  return set_error(QK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return sms;
+}
+
+qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
+                            void* d_planes, uint64_t* d_bad, void* stream) {
+  if (n == 0) return QK_OK;
+  dim3 grid(unsigned(blocks_for(n)), unsigned((p.width_padded + 31) / 32));
+  gate_build_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_angles, n, ld, p.width, p.width_padded, p.front_pad, p.layers == 1 ? 1 : 0,
+      static_cast<double2*>(d_planes), reinterpret_cast<unsigned long long*>(d_bad));
+  return cuda_status(cudaGetLastError(), "gate_build launch");
+}
+
+template <int LAYERS, int MODE, int OUT>
+static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
+  auto kern = sweep_kernel<LAYERS, MODE, OUT>;
+  // per call: the attribute is per device and costs microseconds
+  cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+  if (e != cudaSuccess) return cuda_status(e, "sweep smem attribute");
+  int per_sm = 0;
+  e =
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmemBytes);
+  if (e != cudaSuccess) return cuda_status(e, "sweep occupancy");
+  if (per_sm < 1) per_sm = 1;
+  const int sms = sm_count();
+  if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
+  int64_t grid = int64_t(sms) * per_sm;
+  if (grid > a.n_tiles) grid = a.n_tiles;
+  kern<<<unsigned(grid), kThreads, kSmemBytes, st>>>(a);
+  return cuda_status(cudaGetLastError(), "sweep launch");
+}
+
+qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
+                       const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
+                       double* d_out, int64_t ld_out, int out_mode, void* stream) {
+  if (tile_end <= tile_begin) return QK_OK;
+  SweepArgs a;
+  a.rows = static_cast<const double2*>(d_rows);
+  a.cols = static_cast<const double2*>(d_cols);
+  a.n_rows = n_rows;
+  a.n_cols = n_cols;
+  a.nb_rows = blocks_for(n_rows);
+  a.nb_cols = blocks_for(n_cols);
+  a.tile_begin = tile_begin;
+  a.n_tiles = tile_end - tile_begin;
+  a.out = d_out;
+  a.ld_out = ld_out;
+  a.final_scale = p.final_scale;
+  a.n_pad = p.width_padded;
+  a.nchunks = p.width_padded / kChunk;
+  a.convention = p.convention;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool packed = out_mode == QK_OUT_PACKED;
+  if (p.layers == 2) {
+    if (mode == kModeGram)
+      return packed ? launch_sweep_t<2, kModeGram, QK_OUT_PACKED>(a, st)
+                    : launch_sweep_t<2, kModeGram, QK_OUT_DENSE>(a, st);
+    return packed ? launch_sweep_t<2, kModeCross, QK_OUT_PACKED>(a, st)
+                  : launch_sweep_t<2, kModeCross, QK_OUT_DENSE>(a, st);
+  }
+  if (mode == kModeGram)
+    return packed ? launch_sweep_t<1, kModeGram, QK_OUT_PACKED>(a, st)
+                  : launch_sweep_t<1, kModeGram, QK_OUT_DENSE>(a, st);
+  return packed ? launch_sweep_t<1, kModeCross, QK_OUT_PACKED>(a, st)
+                : launch_sweep_t<1, kModeCross, QK_OUT_DENSE>(a, st);
+}
+
+qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
+                        int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
+                        int64_t ld, void* stream) {
+  (void)p;
+  if (tile_end <= tile_begin) return QK_OK;
+  const int64_t nt = tile_end - tile_begin;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (mode == kModeGram)
+    unpack_kernel<kModeGram><<<unsigned(nt), 256, 0, st>>>(
+        d_packed, n_rows, n_rows, blocks_for(n_rows), blocks_for(n_rows), tile_begin, d_K, ld);
+  else
+    unpack_kernel<kModeCross><<<unsigned(nt), 256, 0, st>>>(
+        d_packed, n_rows, n_cols, blocks_for(n_rows), blocks_for(n_cols), tile_begin, d_K, ld);
+  return cuda_status(cudaGetLastError(), "unpack launch");
+}
+
+qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* d_b, int64_t n_b,
+                       const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream) {
+  if (n_pairs == 0) return QK_OK;
+  const unsigned grid = unsigned((n_pairs + 127) / 128);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nchunks = p.width_padded / kChunk;
+  if (p.layers == 2)
+    pairs_kernel<2><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
+                                          static_cast<const double2*>(d_b), n_b, d_pairs,
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
+  else
+    pairs_kernel<1><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
+                                          static_cast<const double2*>(d_b), n_b, d_pairs,
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
+  return cuda_status(cudaGetLastError(), "pairs launch");
+}
+
+qk_status launch_dfma_peak(double* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int sms = sm_count();
+  if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
+  double* d_sink = nullptr;
+  if (cudaError_t e = cudaMalloc(&d_sink, sizeof(double))) return cuda_status(e, "dfma malloc");
+  const int blocks = sms * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_peak_kernel<<<blocks, 256, 0, st>>>(d_sink, 64);  // warm-up
+  cudaEventRecord(e0, st);
+  dfma_peak_kernel<<<blocks, 256, 0, st>>>(d_sink, iters);
+  cudaEventRecord(e1, st);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_sink);
+  if (e != cudaSuccess) return cuda_status(e, "dfma run");
+  const double flops = double(blocks) * 256 * iters * 16 * 8 * 2;
+  *out = flops / (double(ms) * 1e-3);
+  return QK_OK;
+}
+
+}  // namespace qk

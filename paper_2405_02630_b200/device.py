@@ -1,0 +1,147 @@
+"""Device-resident engine calls: torch CUDA tensors in, torch CUDA tensors out.
+
+Thin stream-ordered wrappers over the C ABI (include/qk.h).  torch supplies device memory,
+the current stream and the process group; every FLOP runs in libqk's sm_100a kernels.
+Non-CUDA inputs are rejected — there is no CPU path.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _native
+from .errors import DeviceError, RebindError
+from .planner import SweepPlan
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _require(t: torch.Tensor, name: str, dtype=None) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise DeviceError(f"{name} must be a CUDA tensor (the engine has no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def angles_to_device(x, device=None) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device or x.device, dtype=torch.float64)
+    else:
+        t = torch.as_tensor(x, dtype=torch.float64).to(device or "cuda")
+    return t.contiguous()
+
+
+class Planes:
+    """Per-sample rotation planes in HBM (output of the gate-build kernel)."""
+
+    def __init__(self, plan: SweepPlan, n_samples: int, buf: torch.Tensor, bad: torch.Tensor):
+        self.plan = plan
+        self.n = int(n_samples)
+        self.buf = buf
+        self.bad = bad
+
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def bad_sample(self) -> int | None:
+        """Smallest sample index holding a non-finite angle, or None (synchronises)."""
+        v = int(self.bad.item())
+        return None if v == -1 else v
+
+
+def gate_build(plan: SweepPlan, angles: torch.Tensor, out: torch.Tensor | None = None) -> Planes:
+    """angles [N, width] fp64 (CUDA) -> planes (network.py:283-302 per sample)."""
+    _require(angles, "angles", torch.float64)
+    if angles.dim() != 2 or angles.shape[1] != plan.width:
+        raise RebindError(f"feature vectors of length {angles.shape[-1]} do not match width "
+                          f"{plan.width}")
+    n = angles.shape[0]
+    nbytes = plan.planes_bytes(n)
+    if out is None or out.numel() < nbytes:
+        out = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=angles.device)
+    bad = torch.full((1,), -1, dtype=torch.int64, device=angles.device)
+    _native.check(_native.lib().qk_gate_build(plan.handle, angles.data_ptr(), n, plan.width,
+                                              out.data_ptr(), bad.data_ptr(), _stream()))
+    return Planes(plan, n, out, bad)
+
+
+def gram(planes: Planes, out: torch.Tensor | None = None, tile_begin: int = 0,
+         tile_end: int | None = None, packed: bool = False) -> torch.Tensor:
+    """Train Gram over upper-triangle tiles [tile_begin, tile_end).
+
+    Dense: writes an N x N fp64 matrix (strict upper computed, mirrored, unit diagonal).
+    Packed: returns the tile-major buffer of the range (edge^2 doubles per tile)."""
+    plan, n = planes.plan, planes.n
+    nt = plan.gram_tile_count(n)
+    tile_end = nt if tile_end is None else tile_end
+    edge = plan.tile_edge
+    if out is None:
+        shape = ((tile_end - tile_begin) * edge * edge,) if packed else (n, n)
+        out = torch.empty(shape, dtype=torch.float64, device=planes.buf.device)
+    _require(out, "out", torch.float64)
+    mode = _native.QK_OUT_PACKED if packed else _native.QK_OUT_DENSE
+    _native.check(_native.lib().qk_gram_tiles(plan.handle, planes.ptr(), n, tile_begin,
+                                              tile_end, out.data_ptr(), mode, _stream()))
+    return out
+
+
+def cross(rows: Planes, cols: Planes, out: torch.Tensor | None = None, tile_begin: int = 0,
+          tile_end: int | None = None, packed: bool = False) -> torch.Tensor:
+    """Test-versus-train block K[r][c] over rectangle tiles [tile_begin, tile_end)."""
+    plan = rows.plan
+    nt = plan.cross_tile_count(rows.n, cols.n)
+    tile_end = nt if tile_end is None else tile_end
+    edge = plan.tile_edge
+    if out is None:
+        shape = ((tile_end - tile_begin) * edge * edge,) if packed else (rows.n, cols.n)
+        out = torch.empty(shape, dtype=torch.float64, device=rows.buf.device)
+    _require(out, "out", torch.float64)
+    mode = _native.QK_OUT_PACKED if packed else _native.QK_OUT_DENSE
+    ld = cols.n if not packed else 0
+    _native.check(_native.lib().qk_cross_tiles(plan.handle, rows.ptr(), rows.n, cols.ptr(),
+                                               cols.n, tile_begin, tile_end, out.data_ptr(), ld,
+                                               mode, _stream()))
+    return out
+
+
+def unpack_gram(plan: SweepPlan, packed: torch.Tensor, n: int, tile_begin: int, tile_end: int,
+                K: torch.Tensor) -> torch.Tensor:
+    _require(packed, "packed", torch.float64)
+    _require(K, "K", torch.float64)
+    _native.check(_native.lib().qk_unpack_gram(plan.handle, packed.data_ptr(), n, tile_begin,
+                                               tile_end, K.data_ptr(), _stream()))
+    return K
+
+
+def unpack_cross(plan: SweepPlan, packed: torch.Tensor, n_rows: int, n_cols: int,
+                 tile_begin: int, tile_end: int, K: torch.Tensor) -> torch.Tensor:
+    _require(packed, "packed", torch.float64)
+    _require(K, "K", torch.float64)
+    _native.check(_native.lib().qk_unpack_cross(plan.handle, packed.data_ptr(), n_rows, n_cols,
+                                                tile_begin, tile_end, K.data_ptr(), n_cols,
+                                                _stream()))
+    return K
+
+
+def pair_amplitudes(a: Planes, b: Planes, pairs: torch.Tensor) -> torch.Tensor:
+    """Signed real amplitudes for explicit (p, q) index pairs, input order (engine.py:132)."""
+    _require(pairs, "pairs", torch.int64)
+    pairs = pairs.reshape(-1, 2).contiguous()
+    out = torch.empty(pairs.shape[0], dtype=torch.float64, device=a.buf.device)
+    _native.check(_native.lib().qk_pair_amplitudes(a.plan.handle, a.ptr(), a.n, b.ptr(), b.n,
+                                                   pairs.data_ptr(), pairs.shape[0],
+                                                   out.data_ptr(), _stream()))
+    return out
+
+
+def dfma_peak_flops() -> float:
+    """Measured FP64 FMA issue rate of the current device (FLOP/s, FMA = 2)."""
+    import ctypes
+
+    v = ctypes.c_double(0.0)
+    _native.check(_native.lib().qk_dfma_peak(ctypes.byref(v), _stream()))
+    torch.cuda.synchronize()
+    return float(v.value)

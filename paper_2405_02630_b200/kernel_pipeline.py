@@ -1,0 +1,312 @@
+"""Kernel-matrix pipeline — the north-star boundary (module kernel_pipeline).
+
+Same operation names, argument meaning, orientation and error behaviour as SPEC's
+``kernel_pipeline`` over the reference engine, so precomputed-kernel SVC training,
+one-vs-rest multiclass and accuracy reporting downstream are unchanged:
+
+  * :func:`enumerate_pairs`     SPEC.md:389-397 (1-based, strict upper triangle, row-major)
+  * :func:`symmetrize`          SPEC.md:398-406 (K + K^T + I, precondition-checked)
+  * :func:`compute_kernel_matrix`  SPEC.md:407-415 (train Gram, diagonal injected as 1.0)
+  * :func:`compute_cross_kernel`   SPEC.md:416-424 (test x train, diagonal computed)
+  * :func:`shard_merge`         SPEC.md:425-434 (deterministic placement, gap/overlap errors)
+
+Underneath, the reference's ``contract_batch`` over a rebind-per-pair network
+(engine.py:132-166) is replaced by libqk: one host sweep plan per structure, a per-sample
+gate-build kernel and the pair-tiled sm_100a sweep.  Host (numpy) inputs go through the
+C-ABI host entry points (H2D, sweep, D2H pipelined over row panels); CUDA torch tensors
+stay on the device.  There is no CPU compute path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from math import ceil
+from typing import Any, Iterable
+
+import numpy as np
+
+from . import _native
+from .config import FeatureMapConfig, as_config, check_convention
+from .errors import RebindError, ShardMergeError, StructuralError
+from .planner import SweepPlan, plan_for
+
+
+@dataclass
+class KernelMatrix:
+    """Dense real kernel block.
+
+    ``entries`` is a row-major float64 ``numpy.ndarray`` of shape (rows, cols) — or a CUDA
+    ``torch.Tensor`` when the inputs were device tensors.
+    """
+
+    rows: int
+    cols: int
+    entries: Any
+    convention: str = "probability"
+    metadata: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        shape = tuple(self.entries.shape)
+        if shape != (self.rows, self.cols):
+            raise StructuralError(f"entries shape {shape} != ({self.rows}, {self.cols})")
+        check_convention(self.convention)
+
+    def to_numpy(self) -> np.ndarray:
+        e = self.entries
+        if isinstance(e, np.ndarray):
+            return e
+        return e.detach().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------------------
+# pair enumeration / symmetrisation / sharding (pure host logic)
+# ---------------------------------------------------------------------------------------
+def enumerate_pairs(n_a: int, n_b: int, symmetric: bool) -> list[tuple[int, int]]:
+    """1-based pair indices: strict upper triangle of n_a x n_a (row-major) when symmetric,
+    else the full n_a x n_b cross product."""
+    if n_a < 1 or n_b < 1:
+        raise ValueError("n_a and n_b must be >= 1")
+    if symmetric:
+        return [(i + 1, j + 1) for i in range(n_a) for j in range(i + 1, n_a)]
+    return [(i + 1, j + 1) for i in range(n_a) for j in range(n_b)]
+
+
+def symmetrize(upper: KernelMatrix) -> KernelMatrix:
+    """K <- K + K^T + I for a strictly-upper matrix (Algorithm 2 step 5)."""
+    if upper.rows != upper.cols:
+        raise StructuralError(f"symmetrize needs a square matrix, got {upper.rows}x{upper.cols}")
+    U = np.asarray(upper.to_numpy(), dtype=np.float64)
+    if np.any(np.tril(U) != 0.0):
+        raise StructuralError("symmetrize precondition violated: strictly-lower or diagonal "
+                              "entries are nonzero (already symmetrised?)")
+    K = U + U.T + np.eye(upper.rows)
+    return KernelMatrix(upper.rows, upper.cols, K, upper.convention, dict(upper.metadata))
+
+
+def shard_range(n_items: int, shard: int, n_shards: int) -> tuple[int, int]:
+    """Contiguous ceil(P/W) shard of a linearised enumeration."""
+    if n_shards < 1 or not 0 <= shard < n_shards:
+        raise ValueError(f"bad shard spec {shard}/{n_shards}")
+    size = ceil(n_items / n_shards) if n_items else 0
+    lo = min(n_items, shard * size)
+    return lo, min(n_items, lo + size)
+
+
+def shard_merge(partials: Iterable[tuple[list, list]], n_a: int | None = None,
+                n_b: int | None = None, symmetric: bool = True,
+                convention: str = "probability", metadata: dict | None = None) -> KernelMatrix:
+    """Place per-shard (pair list, value list) partials by pair index.
+
+    Pair indices are 1-based as produced by :func:`enumerate_pairs`.  Overlaps and gaps in
+    the coverage of the enumeration raise :class:`ShardMergeError` naming the pair.
+    Symmetric merges are symmetrised (K + K^T + I)."""
+    parts = [(list(p), list(v)) for p, v in partials]
+    for k, (p, v) in enumerate(parts):
+        if len(p) != len(v):
+            raise ShardMergeError(f"shard {k}: {len(p)} pairs but {len(v)} values")
+    allp = [pq for p, _ in parts for pq in p]
+    if n_a is None:
+        n_a = max((max(i, j) if symmetric else i) for i, j in allp) if allp else 1
+    if n_b is None:
+        n_b = n_a if symmetric else (max(j for _, j in allp) if allp else 1)
+    K = np.zeros((n_a, n_b))
+    seen = np.zeros((n_a, n_b), dtype=bool)
+    for p, v in parts:
+        for (i, j), val in zip(p, v):
+            if not (1 <= i <= n_a and 1 <= j <= n_b) or (symmetric and i >= j):
+                raise ShardMergeError(f"pair ({i}, {j}) is outside the enumeration")
+            if seen[i - 1, j - 1]:
+                raise ShardMergeError(f"shards overlap at pair ({i}, {j})")
+            seen[i - 1, j - 1] = True
+            K[i - 1, j - 1] = val
+    mask = np.triu(np.ones((n_a, n_b), dtype=bool), k=1) if symmetric else \
+        np.ones((n_a, n_b), dtype=bool)
+    missing = np.argwhere(mask & ~seen)
+    if len(missing):
+        i, j = missing[0]
+        raise ShardMergeError(f"shards leave a gap at pair ({i + 1}, {j + 1}) "
+                              f"({len(missing)} missing)")
+    km = KernelMatrix(n_a, n_b, K, convention, dict(metadata or {}))
+    return symmetrize(km) if symmetric else km
+
+
+# ---------------------------------------------------------------------------------------
+# compute entry points
+# ---------------------------------------------------------------------------------------
+def _resolve_plan(cfg: FeatureMapConfig, plan, convention: str) -> SweepPlan:
+    if isinstance(plan, SweepPlan):
+        if (plan.width, plan.layers, plan.convention) != (cfg.width, cfg.layers, convention):
+            raise StructuralError(
+                f"plan for (width={plan.width}, layers={plan.layers}, {plan.convention}) does "
+                f"not match config (width={cfg.width}, layers={cfg.layers}, {convention})")
+        return plan
+    # None or a reference PlanOptions: the sweep order is structural, options do not apply.
+    return plan_for(cfg, convention)
+
+
+def _check_workers(workers) -> None:
+    if int(workers) < 1:
+        raise ValueError("workers must be >= 1")
+
+
+def _is_cuda_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _host_angles(x, width: int) -> np.ndarray:
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.ndim == 1 and a.size == 0:
+        a = a.reshape(0, width)
+    if a.ndim != 2:
+        raise RebindError(f"operand set 0: expected a 2-D feature array, got shape {a.shape}")
+    return a
+
+
+def _width_error(w_a: int, w_b: int, width: int) -> RebindError:
+    # engine.py:139-144
+    return RebindError(f"operand set 0: vectors of lengths {w_a}/{w_b} do not match width "
+                       f"{width}")
+
+
+def _first_bad_gram_pair(X: np.ndarray) -> int:
+    bad = np.flatnonzero(~np.isfinite(X).all(axis=1))
+    s = int(bad[0])
+    return 0 if s == 0 else s - 1  # pair (0, s) is the first containing s, row-major
+
+
+def _first_bad_cross_pair(T: np.ndarray, R: np.ndarray) -> int:
+    cands = []
+    bt = np.flatnonzero(~np.isfinite(T).all(axis=1))
+    br = np.flatnonzero(~np.isfinite(R).all(axis=1))
+    if len(bt):
+        cands.append(int(bt[0]) * R.shape[0])
+    if len(br):
+        cands.append(int(br[0]))
+    return min(cands)
+
+
+def _metadata(cfg: FeatureMapConfig, plan: SweepPlan, dataset_id, kind: str) -> dict:
+    return {"qubits": cfg.width, "layers": cfg.layers, "dataset": dataset_id,
+            "config_hash": cfg.config_hash(), "kind": kind, "engine": "libqk sm_100a",
+            "plan": dict(plan.info)}
+
+
+def compute_kernel_matrix(features, cfg, plan=None, workers: int = 1, *,
+                          convention: str = "probability", dataset_id: str | None = None,
+                          out: np.ndarray | None = None) -> KernelMatrix:
+    """Train Gram matrix K(x_i, x_j) = |<0|U(x_i)^dag U(x_j)|0>|^2.
+
+    The strict upper triangle is contracted, mirrored, and the diagonal injected as exactly
+    1.0.  ``plan`` may be None, a :class:`SweepPlan`, or the reference's PlanOptions (the
+    sweep order is structural, so path options do not apply).  ``workers`` is accepted for
+    signature compatibility (>= 1); one process drives one GPU — multi-GPU runs go through
+    :mod:`paper_2405_02630_b200.distributed`.  ``out`` may supply a preallocated (e.g.
+    pinned) C-contiguous float64 (N, N) host array to receive the entries."""
+    cfg = as_config(cfg)
+    convention = check_convention(convention)
+    _check_workers(workers)
+    sp = _resolve_plan(cfg, plan, convention)
+    if _is_cuda_tensor(features):
+        return _compute_kernel_matrix_device(features, cfg, sp, convention, dataset_id)
+    X = _host_angles(features, cfg.width)
+    N = X.shape[0]
+    if N >= 2 and X.shape[1] != cfg.width:
+        raise _width_error(X.shape[1], X.shape[1], cfg.width)
+    if out is None:
+        out = np.empty((N, N), dtype=np.float64)
+    elif out.shape != (N, N) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape ({N}, {N})")
+    if N == 1:
+        out[0, 0] = 1.0
+    elif N >= 2:
+        status = _native.lib().qk_kernel_matrix_host(sp.handle, X.ctypes.data, N,
+                                                     out.ctypes.data)
+        if status == _native.QK_ERR_REBIND:
+            raise RebindError(f"operand set {_first_bad_gram_pair(X)}: feature angles must be "
+                              "finite")
+        _native.check(status)
+    return KernelMatrix(N, N, out, convention, _metadata(cfg, sp, dataset_id, "gram"))
+
+
+def compute_cross_kernel(test, train, cfg, plan=None, workers: int = 1, *,
+                         convention: str = "probability", dataset_id: str | None = None,
+                         out: np.ndarray | None = None) -> KernelMatrix:
+    """Test-versus-train block K[r][c] = k(test_r, train_c).
+
+    Full rectangle, rows = test, no symmetrisation, diagonal computed (not injected)."""
+    cfg = as_config(cfg)
+    convention = check_convention(convention)
+    _check_workers(workers)
+    sp = _resolve_plan(cfg, plan, convention)
+    if _is_cuda_tensor(test) or _is_cuda_tensor(train):
+        return _compute_cross_kernel_device(test, train, cfg, sp, convention, dataset_id)
+    T = _host_angles(test, cfg.width)
+    R = _host_angles(train, cfg.width)
+    Nt, Nr = T.shape[0], R.shape[0]
+    if Nt and Nr and (T.shape[1] != cfg.width or R.shape[1] != cfg.width):
+        raise _width_error(T.shape[1], R.shape[1], cfg.width)
+    if out is None:
+        out = np.empty((Nt, Nr), dtype=np.float64)
+    elif out.shape != (Nt, Nr) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape ({Nt}, {Nr})")
+    if Nt and Nr:
+        status = _native.lib().qk_cross_kernel_host(sp.handle, T.ctypes.data, Nt,
+                                                     R.ctypes.data, Nr, out.ctypes.data)
+        if status == _native.QK_ERR_REBIND:
+            raise RebindError(f"operand set {_first_bad_cross_pair(T, R)}: feature angles "
+                              "must be finite")
+        _native.check(status)
+    return KernelMatrix(Nt, Nr, out, convention, _metadata(cfg, sp, dataset_id, "cross"))
+
+
+# ---------------------------------------------------------------------------------------
+# device-resident variants (CUDA torch tensors in -> CUDA torch tensor entries)
+# ---------------------------------------------------------------------------------------
+def _compute_kernel_matrix_device(features, cfg, sp, convention, dataset_id) -> KernelMatrix:
+    import torch
+
+    from . import device as dev
+
+    X = dev.angles_to_device(features)
+    if X.dim() != 2:
+        raise RebindError(f"operand set 0: expected a 2-D feature array, got shape "
+                          f"{tuple(X.shape)}")
+    N = X.shape[0]
+    if N >= 2 and X.shape[1] != cfg.width:
+        raise _width_error(X.shape[1], X.shape[1], cfg.width)
+    if N < 2:
+        K = torch.ones((N, N), dtype=torch.float64, device=X.device)
+        return KernelMatrix(N, N, K, convention, _metadata(cfg, sp, dataset_id, "gram"))
+    planes = dev.gate_build(sp, X)
+    K = dev.gram(planes)
+    bad = planes.bad_sample()
+    if bad is not None:
+        raise RebindError(f"operand set {0 if bad == 0 else bad - 1}: feature angles must be "
+                          "finite")
+    return KernelMatrix(N, N, K, convention, _metadata(cfg, sp, dataset_id, "gram"))
+
+
+def _compute_cross_kernel_device(test, train, cfg, sp, convention, dataset_id) -> KernelMatrix:
+    import torch
+
+    from . import device as dev
+
+    T = dev.angles_to_device(test)
+    R = dev.angles_to_device(train, device=T.device)
+    Nt, Nr = T.shape[0], R.shape[0]
+    if Nt and Nr and (T.shape[1] != cfg.width or R.shape[1] != cfg.width):
+        raise _width_error(T.shape[1], R.shape[1], cfg.width)
+    if not (Nt and Nr):
+        K = torch.empty((Nt, Nr), dtype=torch.float64, device=T.device)
+        return KernelMatrix(Nt, Nr, K, convention, _metadata(cfg, sp, dataset_id, "cross"))
+    pt = dev.gate_build(sp, T)
+    pr = dev.gate_build(sp, R)
+    K = dev.cross(pt, pr)
+    bt, br = pt.bad_sample(), pr.bad_sample()
+    if bt is not None or br is not None:
+        cands = ([bt * Nr] if bt is not None else []) + ([br] if br is not None else [])
+        raise RebindError(f"operand set {min(cands)}: feature angles must be finite")
+    return KernelMatrix(Nt, Nr, K, convention, _metadata(cfg, sp, dataset_id, "cross"))

@@ -1,0 +1,217 @@
+"""Parity of the sm_100a engine (through the C ABI / public API) against the reference golden
+vectors and the oracle.  Gates: |K_gpu - K_ref| <= 1e-12 absolute,
+|amp_gpu - amp_ref| <= 1e-9 |amp_ref| + 1e-300, Gram diagonal exactly 1, Gram exactly symmetric,
+identical SVC predictions."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle  # noqa: E402
+from paper_2405_02630_b200 import (FeatureMapConfig, RebindError, SweepPlan,  # noqa: E402
+                                   compute_cross_kernel, compute_kernel_matrix, contract_batch)
+from paper_2405_02630_b200 import device as dev  # noqa: E402
+from paper_2405_02630_b200.distributed import KernelJob  # noqa: E402
+
+K_ABS = 1e-12
+AMP_REL = 1e-9
+
+L2_CASES = [c for c in GOLDEN_CASES if int(load_golden(c)["layers"]) <= 2]
+
+
+def _amp_ok(amp, ref):
+    return np.all(np.abs(amp - ref) <= AMP_REL * np.abs(ref) + 1e-300)
+
+
+@pytest.mark.parametrize("name", L2_CASES)
+def test_pair_amplitudes_match_reference_golden(name):
+    g = load_golden(name)
+    L = int(g["layers"])
+    plan = SweepPlan(g["A"].shape[1], L)
+    A = torch.as_tensor(g["A"], device="cuda")
+    B = torch.as_tensor(g["B"], device="cuda")
+    pairs = torch.as_tensor(g["pairs"], device="cuda")
+    amp = dev.pair_amplitudes(dev.gate_build(plan, A), dev.gate_build(plan, B), pairs)
+    amp = amp.cpu().numpy()
+    ref = g["amp_re"]
+    assert np.abs(amp ** 2 - ref ** 2).max() <= K_ABS
+    assert _amp_ok(amp, ref)
+
+
+@pytest.mark.parametrize("name", [c for c in L2_CASES if c.startswith(("gram", "cross"))])
+def test_public_api_matches_reference_golden(name):
+    g = load_golden(name)
+    cfg = FeatureMapConfig(g["A"].shape[1], layers=int(g["layers"]))
+    if str(g["kind"]) == "gram":
+        K = compute_kernel_matrix(g["A"], cfg).entries
+        assert np.all(np.diag(K) == 1.0) and np.array_equal(K, K.T)
+    else:
+        K = compute_cross_kernel(g["A"], g["B"], cfg).entries
+    assert np.abs(K - g["K"]).max() <= K_ABS
+
+
+def test_contract_batch_dropin_matches_reference():
+    g = load_golden("pairs_n50_L2")
+    ops = [(g["A"][p], g["B"][q]) for p, q in g["pairs"]]
+    amps = contract_batch(FeatureMapConfig(50), ops)
+    assert all(isinstance(a, complex) and a.imag == 0.0 for a in amps)
+    assert _amp_ok(np.array([a.real for a in amps]), g["amp_re"])
+    assert contract_batch(FeatureMapConfig(50), []) == []
+    with pytest.raises(RebindError, match="operand set 1"):
+        contract_batch(FeatureMapConfig(50), [ops[0], (ops[1][0][:49], ops[1][1])])
+
+
+def test_tile_sweep_and_pair_kernel_are_bit_identical(rng):
+    n = 784
+    X = rng.uniform(0, np.pi, (130, n)) * 0.05 + rng.uniform(0, np.pi, n)
+    plan = SweepPlan(n, 2)
+    Xd = torch.as_tensor(X, device="cuda")
+    planes = dev.gate_build(plan, Xd)
+    K = dev.gram(planes).cpu().numpy()
+    i, j = np.triu_indices(130, 1)
+    pairs = torch.as_tensor(np.stack([i, j], 1), device="cuda")
+    amp = dev.pair_amplitudes(planes, planes, pairs).cpu().numpy()
+    assert np.array_equal(K[i, j], amp * amp)
+
+
+@pytest.mark.parametrize("n,N", [(1, 5), (2, 3), (15, 66), (16, 64), (17, 65), (33, 129),
+                                 (50, 200), (784, 70)])
+def test_gram_and_cross_vs_oracle_edge_sizes(n, N, rng):
+    centre = rng.uniform(0, np.pi, n)
+    X = centre + rng.normal(0, 0.6 / np.sqrt(n), (N, n))
+    T = centre + rng.normal(0, 0.6 / np.sqrt(n), (7, n))
+    for L in (1, 2):
+        cfg = FeatureMapConfig(n, layers=L)
+        K = compute_kernel_matrix(X, cfg).entries
+        Kx = compute_cross_kernel(T, X, cfg).entries
+        assert np.abs(K - oracle.kernel_matrix(X, L)).max() <= K_ABS
+        assert np.abs(Kx - oracle.cross_kernel(T, X, L)).max() <= K_ABS
+        assert np.all(np.diag(K) == 1.0) and np.array_equal(K, K.T)
+
+
+def test_magnitude_convention(rng):
+    X = rng.uniform(0, 0.4, (40, 12))
+    K = compute_kernel_matrix(X, FeatureMapConfig(12), convention="magnitude").entries
+    assert np.abs(K - oracle.kernel_matrix(X, 2, "magnitude")).max() <= K_ABS
+
+
+def test_cross_with_itself_equals_gram(rng):
+    X = rng.uniform(0, 0.5, (90, 30))
+    cfg = FeatureMapConfig(30)
+    K = compute_kernel_matrix(X, cfg).entries
+    Kx = compute_cross_kernel(X, X, cfg).entries
+    assert np.abs(Kx - K).max() <= 1e-12
+    assert np.all(np.abs(np.diag(Kx) - 1.0) <= 1e-9)
+
+
+def test_trivial_sizes_and_errors():
+    cfg = FeatureMapConfig(4)
+    assert compute_kernel_matrix(np.zeros((0, 4)), cfg).entries.shape == (0, 0)
+    assert compute_kernel_matrix(np.zeros((1, 4)), cfg).entries.tolist() == [[1.0]]
+    assert np.all(compute_kernel_matrix(np.ones((4, 4)), cfg).entries == 1.0)
+    with pytest.raises(RebindError, match="operand set 0: vectors of lengths 3/3"):
+        compute_kernel_matrix(np.zeros((3, 3)), cfg)
+    X = np.zeros((6, 4))
+    X[3, 2] = np.nan
+    with pytest.raises(RebindError, match="operand set 2: feature angles must be finite"):
+        compute_kernel_matrix(X, cfg)
+    T = np.zeros((2, 4))
+    T[1, 0] = np.inf
+    with pytest.raises(RebindError, match="operand set 6: feature angles must be finite"):
+        compute_cross_kernel(T, np.zeros((6, 4)), cfg)
+
+
+def test_one_qubit_closed_form():
+    # n = 1, features {0, pi} -> off-diagonal cos^2(pi/2) = 0 (SPEC.md kernel_pipeline example)
+    K = compute_kernel_matrix(np.array([[0.0], [np.pi]]), FeatureMapConfig(1, layers=1)).entries
+    assert abs(K[0, 1]) <= 1e-30 and K[0, 0] == 1.0
+
+
+def test_device_tensor_path_and_packed_unpack(rng):
+    n, N = 64, 300
+    X = torch.as_tensor(rng.uniform(0, 0.3, (N, n)), device="cuda")
+    cfg = FeatureMapConfig(n)
+    K_dev = compute_kernel_matrix(X, cfg).entries
+    K_host = compute_kernel_matrix(X.cpu().numpy(), cfg).entries
+    assert isinstance(K_dev, torch.Tensor) and K_dev.is_cuda
+    assert np.array_equal(K_dev.cpu().numpy(), K_host)
+    plan = SweepPlan(n, 2)
+    planes = dev.gate_build(plan, X)
+    nt = plan.gram_tile_count(N)
+    K2 = torch.zeros((N, N), dtype=torch.float64, device="cuda")
+    for lo, hi in [(0, nt // 3), (nt // 3, nt)]:
+        packed = dev.gram(planes, tile_begin=lo, tile_end=hi, packed=True)
+        dev.unpack_gram(plan, packed, N, lo, hi, K2)
+    assert torch.equal(K2, K_dev)
+
+
+def test_kernel_job_world1_matches_public_api(rng):
+    n = 96
+    Xtr = rng.uniform(0, 0.25, (257, n))
+    Xte = rng.uniform(0, 0.25, (33, n))
+    plan = SweepPlan(n, 2)
+    job = KernelJob(plan, 257, 33)
+    Ktr, Kx = job.run(torch.as_tensor(Xtr, device="cuda"), torch.as_tensor(Xte, device="cuda"))
+    cfg = FeatureMapConfig(n)
+    assert np.array_equal(Ktr.cpu().numpy(), compute_kernel_matrix(Xtr, cfg).entries)
+    assert np.array_equal(Kx.cpu().numpy(), compute_cross_kernel(Xte, Xtr, cfg).entries)
+
+
+def test_pinned_output_pipeline_matches_pageable(rng):
+    n, N = 128, 700
+    X = rng.uniform(0, 0.2, (N, n))
+    cfg = FeatureMapConfig(n)
+    pinned = torch.empty((N, N), dtype=torch.float64, pin_memory=True).numpy()
+    K1 = compute_kernel_matrix(X, cfg, out=pinned).entries
+    K2 = compute_kernel_matrix(X, cfg).entries
+    assert np.array_equal(K1, K2)
+    T = rng.uniform(0, 0.2, (300, n))
+    pinned_x = torch.empty((300, N), dtype=torch.float64, pin_memory=True).numpy()
+    assert np.array_equal(compute_cross_kernel(T, X, cfg, out=pinned_x).entries,
+                          compute_cross_kernel(T, X, cfg).entries)
+
+
+def test_full_size_gram_properties_and_sampled_parity():
+    """Config-4-sized train Gram (10000 x 10000 at 784 qubits): size-independent properties
+    plus sampled entries against the oracle."""
+    from paper_2405_02630_b200.data import config_data
+
+    Atr, _, _, _ = config_data(4, 10000, 0, "mnist", bw=0.05)
+    cfg = FeatureMapConfig(784)
+    K = compute_kernel_matrix(Atr, cfg).entries
+    assert np.all(np.diag(K) == 1.0)
+    assert np.array_equal(K, K.T)
+    assert K.min() >= 0.0 and K.max() <= 1.0 + 1e-9
+    rng = np.random.default_rng(5)
+    i = rng.integers(0, 10000, 48)
+    j = rng.integers(0, 10000, 48)
+    keep = i != j
+    ref = np.abs(oracle.amplitudes(Atr, Atr, np.stack([i[keep], j[keep]], 1), 2)) ** 2
+    assert np.abs(K[i[keep], j[keep]] - ref).max() <= K_ABS
+    med = np.median(ref)
+    assert 1e-3 <= med <= 0.5  # parity data is not in the concentrated K ~ 0 regime
+
+
+def test_svc_predictions_identical(rng):
+    """Downstream: precomputed-kernel SVC, one-vs-rest, C = 1 — identical predictions from
+    the engine's kernels and the oracle's (config-1-shaped: 8 qubits, 100 x 50)."""
+    from sklearn.multiclass import OneVsRestClassifier
+    from sklearn.svm import SVC
+
+    from paper_2405_02630_b200.data import config_data
+
+    Atr, ytr, Ate, yte = config_data(1, 100, 50, "mnist", features=8, binary=(2, 6))
+    cfg = FeatureMapConfig(8)
+    K = compute_kernel_matrix(Atr, cfg).entries
+    Kx = compute_cross_kernel(Ate, Atr, cfg).entries
+    Kr, Kxr = oracle.kernel_matrix(Atr, 2), oracle.cross_kernel(Ate, Atr, 2)
+    assert np.abs(K - Kr).max() <= K_ABS and np.abs(Kx - Kxr).max() <= K_ABS
+    clf = OneVsRestClassifier(SVC(kernel="precomputed", C=1.0)).fit(K, ytr)
+    clf_r = OneVsRestClassifier(SVC(kernel="precomputed", C=1.0)).fit(Kr, ytr)
+    assert np.array_equal(clf.predict(Kx), clf_r.predict(Kxr))
