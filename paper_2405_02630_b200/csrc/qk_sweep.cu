@@ -16,28 +16,35 @@
 // scale at the end):
 //     S+' = (1 + C) S+ + (b_i + b_j) T+        T-' = (a_j - a_i) S+ - D T+
 //     S-' = (a_i + a_j) S- + D T-              T+' = (b_i - b_j) T- - (1 - C) S-
-// amp = (S+ + T+) 2^-n.  That is 16 FP64 instructions per pair-qubit (2 DMUL, 4 DADD,
-// 10 DFMA) against 24 for the textbook (A_i^T V A_j) o RY(delta) form.
+// amp = (S+ + T+) 2^-n.  That is 16 FP64 instructions per pair-qubit (4 DMUL, 4 DADD,
+// 8 DFMA) against 24 for the textbook (A_i^T V A_j) o RY(delta) form.
 // For L = 1 the amplitude is prod_q cos((x_j - x_i)/2) from half-angle planes.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "qk_internal.h"
 
 namespace qk {
 
-constexpr int kThreads = 256;
+// Thread layout of a tile: kTX threads along j with kRJ j-samples each; along i, RI
+// i-samples per thread (template parameter: RI = 4 -> 256 threads, RI = 2 -> 512 threads).
 constexpr int kTX = 16;                 // threads along j
-constexpr int kTY = kThreads / kTX;     // threads along i
-constexpr int kRI = kTile / kTY;        // i-samples per thread (4)
 constexpr int kRJ = kTile / kTX;        // j-samples per thread (4)
+template <int RI>
+struct Geo {
+  static constexpr int kRI = RI;
+  static constexpr int kTY = kTile / RI;           // threads along i
+  static constexpr int kThreads = kTX * kTY;
+  static constexpr int kWarps = kThreads / 32;
+};
 constexpr int kChunkElems = kChunk * kTile;            // double2 per block-chunk
 constexpr uint32_t kChunkBytes = kChunkElems * 16;     // 16 KB
-constexpr size_t kSmemBytes = size_t(kStages) * 2 * kChunkBytes + kStages * 8;
+constexpr size_t kSmemBytes = size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8;  // ring + full + counters
 
-static_assert(kRI * kTY == kTile && kRJ * kTX == kTile, "tile mapping");
+static_assert(kRJ * kTX == kTile, "tile mapping");
 
 // ------------------------------------------------------------------------------------------
 // PTX helpers: mbarrier + bulk async copy (TMA engine, SASS UBLKCP)
@@ -59,6 +66,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -209,12 +220,15 @@ __global__ void __launch_bounds__(256) gate_build_kernel(const double* __restric
 }
 
 // ------------------------------------------------------------------------------------------
-// Pair-tiled sweep.  Persistent CTAs walk tiles g = tile_begin + blockIdx.x + k*gridDim.x;
-// the (tile, chunk) stream is fed by one thread through a kStages-deep ring of bulk copies
-// (i-block chunk + j-block chunk, 32 KB per stage) completing on an mbarrier.  Each thread
-// owns a kRI x kRJ micro-tile of pairs whose bond states live in registers for the whole
-// qubit sweep; per qubit it reads kRI + kRJ double2 from shared memory (broadcast within
-// the warp) and issues 16 * kRI * kRJ FP64 instructions.
+// Pair-tiled sweep.  Persistent CTAs walk tiles g = tile_begin + blockIdx.x + k*gridDim.x.
+// The (tile, chunk) sequence streams through a kStages-deep shared-memory ring of bulk async
+// copies (TMA engine; i-block chunk + j-block chunk, 32 KB per stage) that complete on the
+// stage's `full` mbarrier.  There is no CTA-wide barrier in the loop and no producer warp: each
+// warp counts itself off a stage when it is done reading it, and the LAST warp to release a
+// stage refills it with the item kStages ahead.  Each thread owns a kRI x kRJ micro-tile of
+// pairs whose bond states stay in registers for the whole qubit sweep; per qubit it reads
+// kRI + kRJ double2 from shared memory (broadcast within the warp) and issues 16 * kRI * kRJ
+// FP64 instructions.
 // ------------------------------------------------------------------------------------------
 struct SweepArgs {
   const double2* rows;
@@ -228,25 +242,21 @@ struct SweepArgs {
   int n_pad, nchunks, convention;
 };
 
-template <int LAYERS, int MODE, int OUT>
-__global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepArgs a) {
+template <int LAYERS, int MODE, int OUT, int RI>
+__global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
   using St = typename BondT<LAYERS>::type;
+  constexpr int kRI = Geo<RI>::kRI, kTY = Geo<RI>::kTY, kWarps = Geo<RI>::kWarps;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(kStages) * 2 * kChunkBytes);
+  int* released = reinterpret_cast<int*>(full + kStages);
 
   const int tid = threadIdx.x;
-  const int tx = tid % kTX, ty = tid / kTX;
+  const int lane = tid % 32;
   const int64_t my_tiles =
       a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nchunks = a.nchunks;
   const int64_t F = my_tiles * nchunks;
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
 
   auto tile_of = [&](int64_t k, int64_t& bi, int64_t& bj) {
     const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepArgs a) {
       bj = g - bi * a.nb_cols;
     }
   };
-  auto issue = [&](int64_t f) {
+  auto issue = [&](int64_t f) {  // fill stage f % kStages with item f
     const int64_t k = f / nchunks;
     const int c = int(f - k * nchunks);
     int64_t bi, bj;
@@ -272,10 +282,17 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepArgs a) {
   };
 
   if (tid == 0) {
-    const int64_t pre = F < kStages - 1 ? F : kStages - 1;
-    for (int64_t f = 0; f < pre; ++f) issue(f);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    fence_mbar_init();
+    for (int64_t f = 0; f < F && f < kStages; ++f) issue(f);
   }
+  __syncthreads();
 
+  // ---------------- compute warps ----------------
+  const int tx = tid % kTX, ty = tid / kTX;
   St st[kRI][kRJ];
   int64_t f = 0;
   for (int64_t k = 0; k < my_tiles; ++k) {
@@ -285,7 +302,6 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepArgs a) {
       for (int c = 0; c < kRJ; ++c) st_init<LAYERS>(st[r][c]);
 
     for (int ch = 0; ch < nchunks; ++ch, ++f) {
-      if (tid == 0 && f + kStages - 1 < F) issue(f + kStages - 1);
       const int stage = int(f % kStages);
       mbar_wait(&full[stage], uint32_t((f / kStages) & 1));
       const double2* sI = sbuf + size_t(stage) * 2 * kChunkElems;
@@ -302,13 +318,20 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepArgs a) {
 #pragma unroll
           for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
       }
+      __syncwarp();  // every lane's reads of this stage have completed
+      if (lane == 0) {
+        // the last warp to release the stage refills it with item f + kStages
+        if (atomicAdd(&released[stage], 1) == kWarps - 1) {
+          released[stage] = 0;
+          if (f + kStages < F) issue(f + kStages);
+        }
+      }
       if (LAYERS == 2 && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0) {
 #pragma unroll
         for (int r = 0; r < kRI; ++r)
 #pragma unroll
           for (int c = 0; c < kRJ; ++c) st_rescale<LAYERS>(st[r][c]);
       }
-      __syncthreads();  // every thread is done with this stage before it is refilled
     }
 
     // ---- epilogue ----
@@ -463,24 +486,39 @@ qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, in
   return cuda_status(cudaGetLastError(), "gate_build launch");
 }
 
-template <int LAYERS, int MODE, int OUT>
-static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
-  auto kern = sweep_kernel<LAYERS, MODE, OUT>;
+template <int LAYERS, int MODE, int OUT, int RI>
+static qk_status launch_sweep_ri(const SweepArgs& a, cudaStream_t st) {
+  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI>;
+  constexpr int threads = Geo<RI>::kThreads;
   // per call: the attribute is per device and costs microseconds
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
   if (e != cudaSuccess) return cuda_status(e, "sweep smem attribute");
   int per_sm = 0;
-  e =
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmemBytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, kSmemBytes);
   if (e != cudaSuccess) return cuda_status(e, "sweep occupancy");
   if (per_sm < 1) per_sm = 1;
   const int sms = sm_count();
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
   int64_t grid = int64_t(sms) * per_sm;
   if (grid > a.n_tiles) grid = a.n_tiles;
-  kern<<<unsigned(grid), kThreads, kSmemBytes, st>>>(a);
+  kern<<<unsigned(grid), threads, kSmemBytes, st>>>(a);
   return cuda_status(cudaGetLastError(), "sweep launch");
+}
+
+// Micro-tile rows per thread: QK_SWEEP_RI=2 selects the 512-thread variant (tuning knob).
+static int sweep_ri() {
+  static int ri = [] {
+    const char* v = getenv("QK_SWEEP_RI");
+    return (v != nullptr && v[0] == '2') ? 2 : 4;
+  }();
+  return ri;
+}
+
+template <int LAYERS, int MODE, int OUT>
+static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
+  if (sweep_ri() == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2>(a, st);
+  return launch_sweep_ri<LAYERS, MODE, OUT, 4>(a, st);
 }
 
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
