@@ -11,7 +11,11 @@ from pathlib import Path
 
 from .errors import CapacityError, DeviceError, NativeLibraryError, RebindError, StructuralError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libqk.so"
+import os
+
+# QK_LIB_PATH selects an alternative in-tree build (kernel-variant tuning); default libqk.so.
+LIB_PATH = Path(os.environ.get("QK_LIB_PATH") or
+                Path(__file__).resolve().parent / "_lib" / "libqk.so")
 HEADER = Path(__file__).resolve().parent.parent / "include" / "qk.h"
 
 QK_OK, QK_ERR_VALUE, QK_ERR_REBIND, QK_ERR_CAPACITY, QK_ERR_STRUCTURAL, QK_ERR_CUDA = range(6)

@@ -106,9 +106,14 @@ __device__ __forceinline__ void bond4_init(Bond4& s) {
   s.tm = 0.0;
 }
 
+// 4 DMUL + 4 DADD + 8 DFMA per pair-qubit.  Six of the DFMAs read three distinct registers;
+// the FP64 pipe issues those at ~2/3 rate unless an operand hits the reuse cache (register-file
+// read bandwidth; measured with tools/rfbench.cu: 0.33 vs 0.49 warp-instr/clk/SMSP).  The
+// alternatives that distribute the sums into FMA chains (4 DMUL + 12 DFMA) have more
+// three-source DFMAs and measured 5-9% slower.
 __device__ __forceinline__ void bond4_step(Bond4& s, double2 vi, double2 vj) {
   const double ai = vi.x, bi = vi.y, aj = vj.x, bj = vj.y;
-  const double c = fma(bi, bj, ai * aj);   // cos(x_j - x_i)
+  const double c = fma(bi, bj, ai * aj);     // cos(x_j - x_i)
   const double d = fma(ai, bj, -(bi * aj));  // sin(x_j - x_i)
   const double s1 = bi + bj, d2 = bi - bj, s2 = ai + aj, d1 = aj - ai;
   const double nsp = fma(s1, s.tp, fma(c, s.sp, s.sp));
