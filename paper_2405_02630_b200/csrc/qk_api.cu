@@ -30,7 +30,7 @@ struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
-  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // angles, planes, K, progress
   size_t cap[4] = {0, 0, 0, 0};
   uint64_t* bad = nullptr;  // [2]: non-finite sample sentinels (rows, cols)
 
@@ -71,15 +71,6 @@ qk_status workspace_for_current(Workspace** out, std::unique_lock<std::mutex>& l
   }
   *out = w;
   return QK_OK;
-}
-
-bool is_pinned(const void* p) {
-  cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return at.type == cudaMemoryTypeHost;
 }
 
 // Reads the non-finite sentinels written by the gate build (after the stream synced) and
@@ -200,9 +191,92 @@ qk_status qk_dfma_peak(double* out_flops_per_s, void* stream) {
 }
 
 // ---- host-buffer pipelines -------------------------------------------------------------
-// Inputs are copied H2D (pinned buffers DMA directly; pageable ones go through the driver's
-// staging), the sweep runs on the workspace stream, and the result is copied back.  The
-// Gram is produced in row panels so each panel's D2H overlaps the next panel's sweep.
+// H2D of the angles, gate build, ONE persistent sweep launch over every tile, and the D2H of
+// the result overlapped with the sweep: the kernel counts finished tiles per super-row
+// (kGroup tile rows) and a copy stream waits on each counter (cuStreamWaitValue32) before
+// copying that row panel out.  A Gram row is final once its own and all earlier super-rows
+// are done (its lower part mirrors earlier tile rows), and the waits are queued in row
+// order.  Without stream memory operations the D2H follows the sweep.
+
+}  // extern "C"
+
+namespace {
+
+typedef int (*StreamWaitValue32Fn)(cudaStream_t, uintptr_t, uint32_t, unsigned int);
+
+StreamWaitValue32Fn stream_wait_value32() {
+  static StreamWaitValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return StreamWaitValue32Fn(nullptr);
+    }
+    return reinterpret_cast<StreamWaitValue32Fn>(p);
+  }();
+  return fn;
+}
+
+// Launches the sweep over [0, n_tiles) on w->stream and copies row panels of d_K (row-major,
+// n_cols wide) to h_K on w->copy_stream as their super-rows complete.
+qk_status sweep_and_drain(Workspace* w, const Plan& p, int mode, const void* d_rows,
+                          int64_t n_rows, const void* d_cols, int64_t n_cols, double* d_K,
+                          double* h_K) {
+  const int64_t nbr = blocks_for(n_rows), nbc = blocks_for(n_cols);
+  const int64_t n_super = (nbr + kGroup - 1) / kGroup;
+  const int64_t n_tiles = mode == kModeGram ? nbr * (nbr + 1) / 2 : nbr * nbc;
+  StreamWaitValue32Fn wait = stream_wait_value32();
+  unsigned int* d_prog = nullptr;
+  if (wait != nullptr) {
+    if (qk_status s = w->ensure(3, size_t(n_super) * sizeof(unsigned int))) return s;
+    d_prog = static_cast<unsigned int*>(w->buf[3]);
+    if (cudaError_t e = cudaMemsetAsync(d_prog, 0, size_t(n_super) * 4, w->stream))
+      return cuda_err(e, "progress reset");
+  }
+  cudaEvent_t launched;
+  cudaEventCreateWithFlags(&launched, cudaEventDisableTiming);
+  if (qk_status s = launch_sweep(p, mode, d_rows, n_rows, d_cols, n_cols, 0, n_tiles, d_K,
+                                 n_cols, QK_OUT_DENSE, w->stream, d_prog)) {
+    cudaEventDestroy(launched);
+    return s;
+  }
+  cudaError_t e = cudaSuccess;
+  if (d_prog != nullptr) {
+    // the copy stream must not start waiting before the counters were reset
+    cudaEventRecord(launched, w->stream);
+    cudaStreamWaitEvent(w->copy_stream, launched, 0);
+    cudaStreamQuery(w->stream);  // flush the launch to the device before blocking copies
+    for (int64_t sr = 0; sr < n_super && e == cudaSuccess; ++sr) {
+      const int64_t r0 = sr * kGroup, r1 = std::min<int64_t>(r0 + kGroup, nbr);
+      const uint32_t expect = uint32_t(mode == kModeGram
+                                           ? upper_row_offset(r1, nbr) - upper_row_offset(r0, nbr)
+                                           : (r1 - r0) * nbc);
+      if (wait(w->copy_stream, reinterpret_cast<uintptr_t>(d_prog + sr), expect, 0x0) != 0) {
+        e = cudaErrorNotSupported;
+        break;
+      }
+      const int64_t i0 = r0 * kTile, i1 = std::min<int64_t>(r1 * kTile, n_rows);
+      e = cudaMemcpyAsync(h_K + i0 * n_cols, d_K + i0 * n_cols,
+                          size_t(i1 - i0) * n_cols * sizeof(double), cudaMemcpyDeviceToHost,
+                          w->copy_stream);
+    }
+  } else {
+    e = cudaMemcpyAsync(h_K, d_K, size_t(n_rows) * n_cols * sizeof(double),
+                        cudaMemcpyDeviceToHost, w->stream);
+  }
+  cudaError_t e2 = cudaStreamSynchronize(w->stream);
+  cudaError_t e3 = cudaStreamSynchronize(w->copy_stream);
+  cudaEventDestroy(launched);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = e3;
+  return cuda_err(e, "sweep/D2H pipeline");
+}
+
+}  // namespace
+
+extern "C" {
 
 qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int64_t n_samples,
                                 double* h_K) {
@@ -216,59 +290,19 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
   if (qk_status s = workspace_for_current(&w, lock)) return s;
   const int64_t N = n_samples;
   const size_t xb = size_t(N) * p->width * sizeof(double);
-  const size_t pb = qk_planes_bytes(plan, N);
-  const size_t kb = size_t(N) * size_t(N) * sizeof(double);
   if (qk_status s = w->ensure(0, xb)) return s;
-  if (qk_status s = w->ensure(1, pb)) return s;
-  if (qk_status s = w->ensure(2, kb)) return s;
+  if (qk_status s = w->ensure(1, qk_planes_bytes(plan, N))) return s;
+  if (qk_status s = w->ensure(2, size_t(N) * size_t(N) * sizeof(double))) return s;
   double* dX = static_cast<double*>(w->buf[0]);
-  double* dK = static_cast<double*>(w->buf[2]);
   cudaStream_t st = w->stream;
   if (cudaError_t e = cudaMemcpyAsync(dX, h_angles, xb, cudaMemcpyHostToDevice, st))
     return cuda_err(e, "H2D angles");
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
-
-  // Row panels of whole tile rows; panel k's rows are final once panels 0..k have run
-  // (row i's lower part is the mirror of earlier tile rows).
-  const int64_t nb = blocks_for(N);
-  const int64_t nt = nb * (nb + 1) / 2;
-  const bool pinned = is_pinned(h_K);
-  const int64_t panels = pinned ? std::min<int64_t>(nb, 8) : 1;
-  auto row_off = [nb](int64_t r) { return r * nb - r * (r - 1) / 2; };
-  std::vector<cudaEvent_t> evs;
-  int64_t r0 = 0;
-  for (int64_t k = 0; k < panels; ++k) {
-    // split tile rows so each panel carries ~equal tile counts
-    int64_t r1 = r0;
-    const int64_t target = (nt * (k + 1)) / panels;
-    while (r1 < nb && row_off(r1 + 1) <= target) ++r1;
-    if (k == panels - 1) r1 = nb;
-    if (r1 <= r0) continue;
-    if (qk_status s = launch_sweep(*p, kModeGram, w->buf[1], N, w->buf[1], N, row_off(r0),
-                                   row_off(r1), dK, N, QK_OUT_DENSE, st))
-      return s;
-    const int64_t i0 = r0 * kTile, i1 = std::min<int64_t>(r1 * kTile, N);
-    if (pinned) {
-      cudaEvent_t ev;
-      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      cudaEventRecord(ev, st);
-      cudaStreamWaitEvent(w->copy_stream, ev, 0);
-      evs.push_back(ev);
-      if (cudaError_t e = cudaMemcpyAsync(h_K + i0 * N, dK + i0 * N,
-                                          size_t(i1 - i0) * N * sizeof(double),
-                                          cudaMemcpyDeviceToHost, w->copy_stream))
-        return cuda_err(e, "D2H kernel panel");
-    }
-    r0 = r1;
-  }
-  cudaError_t e = cudaSuccess;
-  if (!pinned) e = cudaMemcpyAsync(h_K, dK, kb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(w->copy_stream);
-  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
-  if (e != cudaSuccess) return cuda_err(e, "kernel matrix pipeline");
+  if (qk_status s = sweep_and_drain(w, *p, kModeGram, w->buf[1], N, w->buf[1], N,
+                                    static_cast<double*>(w->buf[2]), h_K))
+    return s;
   static const char* const names[1] = {"train"};
   return check_bad(w->bad, 1, names);
 }
@@ -287,53 +321,23 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   const size_t xcb = size_t(n_cols) * p->width * sizeof(double);
   const size_t prb = qk_planes_bytes(plan, n_rows);
   const size_t pcb = qk_planes_bytes(plan, n_cols);
-  const size_t kb = size_t(n_rows) * size_t(n_cols) * sizeof(double);
   if (qk_status s = w->ensure(0, xrb + xcb)) return s;
   if (qk_status s = w->ensure(1, prb + pcb)) return s;
-  if (qk_status s = w->ensure(2, kb)) return s;
+  if (qk_status s = w->ensure(2, size_t(n_rows) * size_t(n_cols) * sizeof(double))) return s;
   double* dXr = static_cast<double*>(w->buf[0]);
   double* dXc = dXr + size_t(n_rows) * p->width;
   char* dPr = static_cast<char*>(w->buf[1]);
   char* dPc = dPr + prb;
-  double* dK = static_cast<double*>(w->buf[2]);
   cudaStream_t st = w->stream;
   cudaError_t e = cudaMemcpyAsync(dXr, h_rows, xrb, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dXc, h_cols, xcb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st);
   if (e != cudaSuccess) return cuda_err(e, "H2D angles");
-  if ((e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st)) != cudaSuccess)
-    return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
   if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st)) return s;
-  const int64_t nbr = blocks_for(n_rows), nbc = blocks_for(n_cols);
-  const bool pinned = is_pinned(h_K);
-  const int64_t panels = pinned ? std::min<int64_t>(nbr, 8) : 1;
-  std::vector<cudaEvent_t> evs;
-  int64_t r0 = 0;
-  for (int64_t k = 0; k < panels; ++k) {
-    const int64_t r1 = (k == panels - 1) ? nbr : (nbr * (k + 1)) / panels;
-    if (r1 <= r0) continue;
-    if (qk_status s = launch_sweep(*p, kModeCross, dPr, n_rows, dPc, n_cols, r0 * nbc, r1 * nbc,
-                                   dK, n_cols, QK_OUT_DENSE, st))
-      return s;
-    if (pinned) {
-      const int64_t i0 = r0 * kTile, i1 = std::min<int64_t>(r1 * kTile, n_rows);
-      cudaEvent_t ev;
-      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      cudaEventRecord(ev, st);
-      cudaStreamWaitEvent(w->copy_stream, ev, 0);
-      evs.push_back(ev);
-      e = cudaMemcpyAsync(h_K + i0 * n_cols, dK + i0 * n_cols,
-                          size_t(i1 - i0) * n_cols * sizeof(double), cudaMemcpyDeviceToHost,
-                          w->copy_stream);
-      if (e != cudaSuccess) return cuda_err(e, "D2H cross panel");
-    }
-    r0 = r1;
-  }
-  if (!pinned) e = cudaMemcpyAsync(h_K, dK, kb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(w->copy_stream);
-  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
-  if (e != cudaSuccess) return cuda_err(e, "cross kernel pipeline");
+  if (qk_status s = sweep_and_drain(w, *p, kModeCross, dPr, n_rows, dPc, n_cols,
+                                    static_cast<double*>(w->buf[2]), h_K))
+    return s;
   static const char* const names[2] = {"test", "train"};
   return check_bad(w->bad, 2, names);
 }

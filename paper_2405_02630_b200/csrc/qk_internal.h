@@ -13,6 +13,7 @@ constexpr int kTile = 64;    // samples per plane block == tile edge T
 constexpr int kChunk = 16;   // qubits per bulk-copy chunk Q
 constexpr int kStages = 4;   // shared-memory ring depth
 constexpr int kRescaleChunks = 32;  // L=2: multiply the bond state by 2^-512 every 512 qubits
+constexpr int kGroup = 8;           // tile rows per super-row of the L2-friendly tile order
 
 struct Plan {
   int32_t width = 0;
@@ -29,12 +30,22 @@ qk_status check_plan(const qk_plan* p, const Plan** out);
 
 int64_t blocks_for(int64_t n_samples);
 
+#ifdef __CUDACC__
+#define QK_HD __host__ __device__
+#else
+#define QK_HD
+#endif
+
+// First linear index of tile row r in the upper-triangle tile list over nb blocks.
+QK_HD inline int64_t upper_row_offset(int64_t r, int64_t nb) { return r * nb - r * (r - 1) / 2; }
+
 // Device launchers (qk_sweep.cu).  They return QK_OK or a QK_ERR_CUDA status.
 qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
                             void* d_planes, uint64_t* d_bad, void* stream);
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
-                       double* d_out, int64_t ld_out, int out_mode, void* stream);
+                       double* d_out, int64_t ld_out, int out_mode, void* stream,
+                       unsigned int* d_progress = nullptr);
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
                         int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                         int64_t ld, void* stream);

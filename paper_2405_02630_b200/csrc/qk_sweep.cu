@@ -177,17 +177,49 @@ __device__ __forceinline__ double kernel_value(double amp, int convention) {
   return convention == QK_MAGNITUDE ? fabs(amp) : amp * amp;
 }
 
-// Upper-triangle tile list, row-major over nb plane blocks: row b holds tiles (b, b..nb-1).
-__device__ __forceinline__ void decode_upper(int64_t g, int64_t nb, int64_t& bi, int64_t& bj) {
+// Tile order.  Tiles are grouped into super-rows of kGroup tile rows (the Gram's upper
+// triangle: rows b..nb-1 of each tile row b; the cross rectangle: all nb_cols) and, inside a
+// super-row, walked column by column.  A wave of 148 persistent CTAs then covers ~kGroup tile
+// rows x ~148/kGroup tile columns, whose gate planes (~20 MB at 784 qubits) stay in L2 instead
+// of streaming the whole plane array per wave.  A super-row holds exactly the tiles of its
+// rows, so super-row boundaries coincide with plain row-major offsets (used by the host-side
+// row panels).
+// Row-major position -> tile row (the plain upper-triangle row containing linear index g).
+__host__ __device__ __forceinline__ int64_t upper_row_of(int64_t g, int64_t nb) {
   const double m = 2.0 * double(nb) + 1.0;
   int64_t b = int64_t((m - sqrt(m * m - 8.0 * double(g))) * 0.5);
   if (b < 0) b = 0;
   if (b > nb - 1) b = nb - 1;
-  auto off = [nb](int64_t r) { return r * nb - r * (r - 1) / 2; };
-  while (b > 0 && off(b) > g) --b;
-  while (b + 1 < nb && off(b + 1) <= g) ++b;
-  bi = b;
-  bj = b + (g - off(b));
+  while (b > 0 && upper_row_offset(b, nb) > g) --b;
+  while (b + 1 < nb && upper_row_offset(b + 1, nb) <= g) ++b;
+  return b;
+}
+
+__host__ __device__ __forceinline__ void decode_upper(int64_t g, int64_t nb, int64_t& bi, int64_t& bj) {
+  const int64_t r0 = (upper_row_of(g, nb) / kGroup) * kGroup;
+  const int64_t h = nb - r0 < kGroup ? nb - r0 : kGroup;
+  const int64_t local = g - upper_row_offset(r0, nb);
+  const int64_t tri = h * (h + 1) / 2;
+  if (local < tri) {  // columns r0 .. r0+h-1: column c holds rows r0 .. r0+c
+    int64_t c = int64_t((sqrt(8.0 * double(local) + 1.0) - 1.0) * 0.5);
+    while (c > 0 && c * (c + 1) / 2 > local) --c;
+    while ((c + 1) * (c + 2) / 2 <= local) ++c;
+    bj = r0 + c;
+    bi = r0 + (local - c * (c + 1) / 2);
+  } else {  // columns r0+h .. nb-1: full columns of h rows
+    const int64_t l2 = local - tri;
+    bj = r0 + h + l2 / h;
+    bi = r0 + l2 % h;
+  }
+}
+
+__host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows, int64_t nb_cols,
+                                            int64_t& bi, int64_t& bj) {
+  const int64_t r0 = (g / (kGroup * nb_cols)) * kGroup;
+  const int64_t h = nb_rows - r0 < kGroup ? nb_rows - r0 : kGroup;
+  const int64_t local = g - r0 * nb_cols;
+  bj = local / h;
+  bi = r0 + local % h;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -245,6 +277,7 @@ struct SweepArgs {
   int64_t ld_out;
   double final_scale;
   int n_pad, nchunks, convention;
+  unsigned int* progress;  // optional: per-super-row count of finished tiles (host pipelines)
 };
 
 template <int LAYERS, int MODE, int OUT, int RI>
@@ -268,8 +301,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     if (MODE == kModeGram) {
       decode_upper(g, a.nb_rows, bi, bj);
     } else {
-      bi = g / a.nb_cols;
-      bj = g - bi * a.nb_cols;
+      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
     }
   };
   auto issue = [&](int64_t f) {  // fill stage f % kStages with item f
@@ -374,6 +406,12 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         }
       }
     }
+    if (a.progress != nullptr) {
+      // publish the finished tile to a copy stream waiting on its super-row counter
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) atomicAdd(a.progress + bi / kGroup, 1u);
+    }
   }
 }
 
@@ -423,8 +461,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const double* __restrict__ 
   if (MODE == kModeGram) {
     decode_upper(g, nb_rows, bi, bj);
   } else {
-    bi = g / nb_cols;
-    bj = g - bi * nb_cols;
+    decode_rect(g, nb_rows, nb_cols, bi, bj);
   }
   const double* src = packed + int64_t(blockIdx.x) * kTile * kTile;
   for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
@@ -528,9 +565,11 @@ static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
 
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
-                       double* d_out, int64_t ld_out, int out_mode, void* stream) {
+                       double* d_out, int64_t ld_out, int out_mode, void* stream,
+                       unsigned int* d_progress) {
   if (tile_end <= tile_begin) return QK_OK;
   SweepArgs a;
+  a.progress = d_progress;
   a.rows = static_cast<const double2*>(d_rows);
   a.cols = static_cast<const double2*>(d_cols);
   a.n_rows = n_rows;

@@ -1,0 +1,96 @@
+"""The C ABI (include/qk.h) — loads, exports every declared symbol, validates like the reference
+(FeatureMapConfig checks, circuit.py:86-91) without a GPU, and fails loudly (no CPU fallback)
+when no CUDA device is present."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2405_02630_b200 import (CapacityError, DeviceError, FeatureMapConfig, SweepPlan,
+                                   compute_cross_kernel, compute_kernel_matrix)
+from paper_2405_02630_b200 import _native
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    declared = _native.declared_symbols()
+    assert len(declared) >= 17
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_native._SIGNATURES)
+    assert lib.qk_abi_version() == 1
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("width,layers,conv,exc,msg", [
+    (0, 2, 0, ValueError, "width must be >= 1"),
+    (4, 0, 0, ValueError, "layers must be >= 1"),
+    (4, 2, 7, ValueError, "unknown kernel convention"),
+    (4, 3, 0, CapacityError, "bond-16"),
+])
+def test_plan_validation_through_the_abi(width, layers, conv, exc, msg):
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    status = lib.qk_plan_create(width, layers, conv, ctypes.byref(h))
+    assert status != 0 and not h.value
+    with pytest.raises(exc, match=msg):
+        _native.check(status)
+
+
+def test_plan_geometry_and_costs():
+    p = SweepPlan(784, 2)
+    i = p.info
+    assert (i["bond"], i["tile_edge"], i["chunk"], i["width_padded"]) == (4, 64, 16, 784)
+    assert i["algorithmic_flops_per_entry"] == 34 * 784 + 4
+    assert i["dp_instr_per_entry"] == 16 * 784 + 3
+    assert i["reference_cmacs_per_entry"] == 1056 * 784 - 3912  # reference planner (probe1)
+    assert p.gram_tile_count(10000) == 157 * 158 // 2
+    assert p.cross_tile_count(2000, 10000) == 32 * 157
+    assert p.planes_bytes(10000) == 157 * 784 * 64 * 16
+    q = SweepPlan(17, 2)
+    assert q.info["width_padded"] == 32  # 15 identity qubits in front
+    assert SweepPlan(5, 1).info["bond"] == 1
+
+
+def test_null_and_range_arguments_are_rejected():
+    lib = _native.lib()
+    p = SweepPlan(8, 2)
+    assert lib.qk_gram_tiles(p.handle, None, 100, 0, 10**6, None, 0, None) == _native.QK_ERR_VALUE
+    assert "tile range" in _native.last_error()
+    assert lib.qk_gram_tiles(None, None, 1, 0, 1, None, 0, None) == _native.QK_ERR_VALUE
+    assert lib.qk_cross_tiles(p.handle, None, 10, None, 10, 0, 1, None, 5, 0, None) == \
+        _native.QK_ERR_VALUE  # ld_out < n_cols
+
+
+def _has_cuda() -> bool:
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except ImportError:  # pragma: no cover
+        return False
+
+
+@pytest.mark.skipif(_has_cuda(), reason="checks the no-device failure mode")
+def test_compute_fails_loudly_without_a_device():
+    X = np.random.default_rng(0).uniform(0, 1, (5, 4))
+    with pytest.raises(DeviceError):
+        compute_kernel_matrix(X, FeatureMapConfig(4))
+    with pytest.raises(DeviceError):
+        compute_cross_kernel(X, X, FeatureMapConfig(4))
+
+
+def test_missing_library_is_a_hard_error(tmp_path, monkeypatch):
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setattr(_native, "LIB_PATH", tmp_path / "absent.so")
+    from paper_2405_02630_b200 import NativeLibraryError
+
+    with pytest.raises(NativeLibraryError, match="no CPU fallback"):
+        _native.lib()

@@ -1,0 +1,120 @@
+"""Multi-process (world_size 2, gloo on CPU) check of the tile sharding + gather contract used
+by the multi-GPU path: every tile of the job is owned by exactly one rank, the padded packed
+buffers gather to rank 0, and placing them by (segment, tile) rebuilds the dense matrices.
+The sweeps/unpacks themselves are CUDA kernels (covered by the gpu tests); here each rank
+fills its packed tiles with a known function of the global (i, j) coordinates."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2405_02630_b200 import SweepPlan
+from paper_2405_02630_b200.distributed import gather_packed, layout_for
+
+N_TRAIN, N_TEST, WIDTH = 300, 70, 8
+
+
+def f(i, j):
+    return 1.0 + i * 1e-3 + j * 1e-7
+
+
+def upper_tile(g, nb):
+    r, off = 0, 0
+    while off + (nb - r) <= g:
+        off += nb - r
+        r += 1
+    return r, r + (g - off)
+
+
+def fill(buf, lay, rank, T):
+    for seg in lay.segments(rank):
+        for t in range(seg.tile_begin, seg.tile_end):
+            if seg.kind == "gram":
+                bi, bj = upper_tile(t, -(-lay.n_train // T))
+            else:
+                nbc = -(-lay.n_train // T)
+                bi, bj = divmod(t, nbc)
+            il, jl = np.meshgrid(np.arange(T), np.arange(T), indexing="ij")
+            base = (seg.offset + t - seg.tile_begin) * T * T
+            buf[base:base + T * T] = torch.from_numpy(f(bi * T + il, bj * T + jl).ravel())
+
+
+def place(bufs, lay, T):
+    K = np.zeros((lay.n_train, lay.n_train))
+    Kx = np.zeros((lay.n_test, lay.n_train))
+    nb = -(-lay.n_train // T)
+    for r, buf in enumerate(bufs):
+        b = buf.numpy()
+        for seg in lay.segments(r):
+            for t in range(seg.tile_begin, seg.tile_end):
+                tile = b[(seg.offset + t - seg.tile_begin) * T * T:][:T * T].reshape(T, T)
+                bi, bj = upper_tile(t, nb) if seg.kind == "gram" else divmod(t, nb)
+                for il in range(T):
+                    i = bi * T + il
+                    for jl in range(T):
+                        j = bj * T + jl
+                        if seg.kind == "gram":
+                            if i < j < lay.n_train:
+                                K[i, j] = K[j, i] = tile[il, jl]
+                            elif i == j < lay.n_train:
+                                K[i, i] = 1.0
+                        elif i < lay.n_test and j < lay.n_train:
+                            Kx[i, j] = tile[il, jl]
+    return K, Kx
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = SweepPlan(WIDTH, 2)
+    T = plan.tile_edge
+    lay = layout_for(plan, N_TRAIN, N_TEST, world)
+    buf = torch.full((lay.range_len * lay.tile_elems,), np.nan, dtype=torch.float64)
+    fill(buf, lay, rank, T)
+    bufs = gather_packed(buf, lay)
+    if rank == 0:
+        K, Kx = place(bufs, lay, T)
+        i, j = np.meshgrid(np.arange(N_TRAIN), np.arange(N_TRAIN), indexing="ij")
+        Kref = np.where(i == j, 1.0, f(np.minimum(i, j), np.maximum(i, j)))
+        ti, tj = np.meshgrid(np.arange(N_TEST), np.arange(N_TRAIN), indexing="ij")
+        q.put((bool(np.array_equal(K, Kref)), bool(np.array_equal(Kx, f(ti, tj)))))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_layout_partitions_every_tile_exactly_once():
+    plan = SweepPlan(WIDTH, 2)
+    for world in (1, 2, 3, 8):
+        lay = layout_for(plan, N_TRAIN, N_TEST, world)
+        seen = {"gram": [], "cross": []}
+        for r in range(world):
+            for seg in lay.segments(r):
+                seen[seg.kind].extend(range(seg.tile_begin, seg.tile_end))
+                assert seg.offset + seg.tile_end - seg.tile_begin <= lay.range_len
+        assert seen["gram"] == list(range(lay.gram_tiles))
+        assert seen["cross"] == list(range(lay.cross_tiles))
+    assert lay.entries() == N_TRAIN * (N_TRAIN - 1) // 2 + N_TEST * N_TRAIN
+
+
+@pytest.mark.timeout(300)
+def test_gather_rebuilds_dense_matrices_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert ok == (True, True)
+    assert all(p.exitcode == 0 for p in procs)

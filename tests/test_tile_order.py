@@ -1,0 +1,25 @@
+"""Host-compiled check of the sweep kernel's tile decode (qk_sweep.cu): bijective over the Gram
+upper triangle and the cross rectangle, and super-rows contiguous in tile order (the row
+panels of the host pipeline and the per-rank ranges rely on it)."""
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.skipif(shutil.which("nvcc") is None and not Path("/usr/local/cuda/bin/nvcc").exists(),
+                    reason="needs nvcc")
+def test_tile_decode_is_a_bijection(tmp_path):
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    exe = tmp_path / "tile_order_check"
+    subprocess.run([nvcc, "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+                    "-I", str(ROOT / "include"), "-I", str(ROOT / "paper_2405_02630_b200" / "csrc"),
+                    "-o", str(exe), str(ROOT / "tests" / "native" / "tile_order_check.cu"),
+                    str(ROOT / "paper_2405_02630_b200" / "csrc" / "qk_plan.cpp")],
+                   check=True, capture_output=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    lines = out.strip().splitlines()
+    assert len(lines) == 10 and all(l.endswith(" ok") for l in lines), out
