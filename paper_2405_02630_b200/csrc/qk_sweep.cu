@@ -42,7 +42,9 @@ struct Geo {
 };
 constexpr int kChunkElems = kChunk * kTile;            // double2 per block-chunk
 constexpr uint32_t kChunkBytes = kChunkElems * 16;     // 16 KB
-constexpr size_t kSmemBytes = size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8;  // ring + full + counters
+constexpr int kTileTable = 512;  // per-CTA decoded tile coordinates cached in shared memory
+constexpr size_t kSmemBytes =
+    size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8 + kTileTable * 8;  // ring, barriers, table
 
 static_assert(kRJ * kTX == kTile, "tile mapping");
 
@@ -296,7 +298,8 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   const int nchunks = a.nchunks;
   const int64_t F = my_tiles * nchunks;
 
-  auto tile_of = [&](int64_t k, int64_t& bi, int64_t& bj) {
+  int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
+  auto decode = [&](int64_t k, int64_t& bi, int64_t& bj) {
     const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
     if (MODE == kModeGram) {
       decode_upper(g, a.nb_rows, bi, bj);
@@ -304,6 +307,21 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
     }
   };
+  auto tile_of = [&](int64_t k, int64_t& bi, int64_t& bj) {
+    if (k < kTileTable) {
+      const int2 t = table[k];
+      bi = t.x;
+      bj = t.y;
+    } else {
+      decode(k, bi, bj);
+    }
+  };
+  for (int64_t k = tid; k < my_tiles && k < kTileTable; k += blockDim.x) {
+    int64_t bi, bj;
+    decode(k, bi, bj);
+    table[k] = make_int2(int(bi), int(bj));
+  }
+  __syncthreads();
   auto issue = [&](int64_t f) {  // fill stage f % kStages with item f
     const int64_t k = f / nchunks;
     const int c = int(f - k * nchunks);
