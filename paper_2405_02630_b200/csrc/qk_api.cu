@@ -3,6 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -33,6 +37,26 @@ struct Workspace {
   void* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // angles, planes, K, progress
   size_t cap[4] = {0, 0, 0, 0};
   uint64_t* bad = nullptr;  // [2]: non-finite sample sentinels (rows, cols)
+  void* stage[2] = {nullptr, nullptr};  // pinned staging for pageable host buffers
+  size_t stage_cap = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+
+  qk_status ensure_stage(size_t bytes) {
+    if (stage_cap >= bytes) return QK_OK;
+    for (int k = 0; k < 2; ++k) {
+      if (stage[k]) cudaFreeHost(stage[k]);
+      stage[k] = nullptr;
+    }
+    stage_cap = 0;
+    for (int k = 0; k < 2; ++k) {
+      if (cudaError_t e = cudaHostAlloc(&stage[k], bytes, cudaHostAllocDefault))
+        return set_error(QK_ERR_CAPACITY, std::string("pinned staging allocation failed: ") +
+                                              cudaGetErrorString(e));
+      if (!stage_ev[k]) cudaEventCreateWithFlags(&stage_ev[k], cudaEventDisableTiming);
+    }
+    stage_cap = bytes;
+    return QK_OK;
+  }
 
   qk_status ensure(int slot, size_t bytes) {
     if (cap[slot] >= bytes) return QK_OK;
@@ -83,6 +107,112 @@ qk_status check_bad(const uint64_t* d_bad, int count, const char* const* names) 
     if (h[k] != UINT64_MAX)
       return set_error(QK_ERR_REBIND, std::string("feature angles must be finite (") + names[k] +
                                           " sample " + std::to_string(h[k]) + ")");
+  return QK_OK;
+}
+
+
+// Small persistent pool for host-side memcpy between pageable user buffers and the pinned
+// staging buffers (parallel copies also parallelise first-touch page faults).
+class CopyPool {
+ public:
+  CopyPool() {
+    unsigned n = std::thread::hardware_concurrency();
+    n = std::max(1u, std::min(16u, n));
+    for (unsigned k = 0; k < n; ++k) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  // copies n bytes src -> dst in parallel; blocks until done
+  void copy(void* dst, const void* src, size_t n) {
+    const size_t parts = std::min<size_t>(workers_.size(), std::max<size_t>(1, n >> 22));
+    if (parts <= 1) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    std::lock_guard<std::mutex> one_caller(call_mu_);
+    std::unique_lock<std::mutex> g(mu_);
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    n_ = n;
+    parts_ = parts;
+    next_ = 0;
+    done_ = 0;
+    ++gen_;
+    cv_.notify_all();
+    done_cv_.wait(g, [this] { return done_ == parts_; });
+  }
+
+ private:
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> g(mu_);
+    for (;;) {
+      cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      while (next_ < parts_) {
+        const size_t k = next_++;
+        const size_t lo = n_ * k / parts_, hi = n_ * (k + 1) / parts_;
+        char* d = dst_;
+        const char* sp = src_;
+        g.unlock();
+        std::memcpy(d + lo, sp + lo, hi - lo);
+        g.lock();
+        if (++done_ == parts_) done_cv_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  bool stop_ = false;
+  uint64_t gen_ = 0;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t n_ = 0, parts_ = 0, next_ = 0, done_ = 0;
+};
+
+CopyPool& copy_pool() {
+  static CopyPool pool;
+  return pool;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Host -> device on w->stream: pinned sources DMA directly; pageable ones go through the
+// pinned staging pair (parallel memcpy into one slot while the other is in flight).
+qk_status upload(Workspace* w, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return QK_OK;
+  if (is_pinned(src))
+    return cuda_err(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, w->stream), "H2D");
+  const size_t chunk = size_t(64) << 20;
+  if (qk_status s = w->ensure_stage(chunk)) return s;
+  bool used[2] = {false, false};
+  size_t k = 0;
+  for (size_t off = 0; off < bytes; off += chunk, ++k) {
+    const int slot = int(k & 1);
+    const size_t n = std::min(chunk, bytes - off);
+    if (used[slot]) cudaEventSynchronize(w->stage_ev[slot]);
+    copy_pool().copy(w->stage[slot], static_cast<const char*>(src) + off, n);
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, w->stage[slot], n,
+                                    cudaMemcpyHostToDevice, w->stream);
+    if (e != cudaSuccess) return cuda_err(e, "H2D staged");
+    cudaEventRecord(w->stage_ev[slot], w->stream);
+    used[slot] = true;
+  }
   return QK_OK;
 }
 
@@ -227,6 +357,11 @@ qk_status sweep_and_drain(Workspace* w, const Plan& p, int mode, const void* d_r
   const int64_t nbr = blocks_for(n_rows), nbc = blocks_for(n_cols);
   const int64_t n_super = (nbr + kGroup - 1) / kGroup;
   const int64_t n_tiles = mode == kModeGram ? nbr * (nbr + 1) / 2 : nbr * nbc;
+  const bool pinned = is_pinned(h_K);
+  const size_t row_bytes = size_t(n_cols) * sizeof(double);
+  const size_t panel_bytes = size_t(kGroup) * kTile * row_bytes;
+  if (!pinned)
+    if (qk_status s = w->ensure_stage(panel_bytes)) return s;
   StreamWaitValue32Fn wait = stream_wait_value32();
   unsigned int* d_prog = nullptr;
   if (wait != nullptr) {
@@ -235,40 +370,78 @@ qk_status sweep_and_drain(Workspace* w, const Plan& p, int mode, const void* d_r
     if (cudaError_t e = cudaMemsetAsync(d_prog, 0, size_t(n_super) * 4, w->stream))
       return cuda_err(e, "progress reset");
   }
-  cudaEvent_t launched;
-  cudaEventCreateWithFlags(&launched, cudaEventDisableTiming);
+  // the copy stream may start waiting on the counters once they are reset (NOT once the
+  // sweep finished: the event is recorded before the launch)
+  cudaEvent_t reset;
+  cudaEventCreateWithFlags(&reset, cudaEventDisableTiming);
+  cudaEventRecord(reset, w->stream);
   if (qk_status s = launch_sweep(p, mode, d_rows, n_rows, d_cols, n_cols, 0, n_tiles, d_K,
                                  n_cols, QK_OUT_DENSE, w->stream, d_prog)) {
-    cudaEventDestroy(launched);
+    cudaEventDestroy(reset);
     return s;
   }
-  cudaError_t e = cudaSuccess;
+  cudaStream_t cs = w->copy_stream;
+  if (!pinned) {  // the staging slots may still feed the H2D of the inputs
+    for (int k = 0; k < 2; ++k)
+      if (w->stage_ev[k]) cudaStreamWaitEvent(cs, w->stage_ev[k], 0);
+  }
   if (d_prog != nullptr) {
-    // the copy stream must not start waiting before the counters were reset
-    cudaEventRecord(launched, w->stream);
-    cudaStreamWaitEvent(w->copy_stream, launched, 0);
-    cudaStreamQuery(w->stream);  // flush the launch to the device before blocking copies
-    for (int64_t sr = 0; sr < n_super && e == cudaSuccess; ++sr) {
+    cudaStreamWaitEvent(cs, reset, 0);
+  } else {
+    cudaEvent_t fin;  // no stream memory ops: drain after the sweep
+    cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+    cudaEventRecord(fin, w->stream);
+    cudaStreamWaitEvent(cs, fin, 0);
+    cudaEventDestroy(fin);
+  }
+  cudaStreamQuery(w->stream);  // flush the launch to the device before host-blocking work
+  cudaError_t e = cudaSuccess;
+  auto rows_of = [&](int64_t sr, int64_t& i0, int64_t& i1) {
+    i0 = sr * kGroup * kTile;
+    i1 = std::min<int64_t>((sr + 1) * kGroup * kTile, n_rows);
+  };
+  auto enqueue = [&](int64_t sr, void* dst) -> cudaError_t {
+    if (d_prog != nullptr) {
       const int64_t r0 = sr * kGroup, r1 = std::min<int64_t>(r0 + kGroup, nbr);
       const uint32_t expect = uint32_t(mode == kModeGram
                                            ? upper_row_offset(r1, nbr) - upper_row_offset(r0, nbr)
                                            : (r1 - r0) * nbc);
-      if (wait(w->copy_stream, reinterpret_cast<uintptr_t>(d_prog + sr), expect, 0x0) != 0) {
-        e = cudaErrorNotSupported;
-        break;
-      }
-      const int64_t i0 = r0 * kTile, i1 = std::min<int64_t>(r1 * kTile, n_rows);
-      e = cudaMemcpyAsync(h_K + i0 * n_cols, d_K + i0 * n_cols,
-                          size_t(i1 - i0) * n_cols * sizeof(double), cudaMemcpyDeviceToHost,
-                          w->copy_stream);
+      if (wait(cs, reinterpret_cast<uintptr_t>(d_prog + sr), expect, 0x0) != 0)
+        return cudaErrorNotSupported;
+    }
+    int64_t i0, i1;
+    rows_of(sr, i0, i1);
+    return cudaMemcpyAsync(dst, d_K + i0 * n_cols, size_t(i1 - i0) * row_bytes,
+                           cudaMemcpyDeviceToHost, cs);
+  };
+  if (pinned) {
+    for (int64_t sr = 0; sr < n_super && e == cudaSuccess; ++sr) {
+      int64_t i0, i1;
+      rows_of(sr, i0, i1);
+      e = enqueue(sr, h_K + i0 * n_cols);
     }
   } else {
-    e = cudaMemcpyAsync(h_K, d_K, size_t(n_rows) * n_cols * sizeof(double),
-                        cudaMemcpyDeviceToHost, w->stream);
+    // two pinned slots: DMA panel sr+2 while the pool copies panel sr into the user buffer
+    for (int64_t sr = 0; sr < std::min<int64_t>(2, n_super) && e == cudaSuccess; ++sr) {
+      e = enqueue(sr, w->stage[sr & 1]);
+      if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[sr & 1], cs);
+    }
+    for (int64_t sr = 0; sr < n_super && e == cudaSuccess; ++sr) {
+      const int slot = int(sr & 1);
+      e = cudaEventSynchronize(w->stage_ev[slot]);
+      if (e != cudaSuccess) break;
+      int64_t i0, i1;
+      rows_of(sr, i0, i1);
+      copy_pool().copy(h_K + i0 * n_cols, w->stage[slot], size_t(i1 - i0) * row_bytes);
+      if (sr + 2 < n_super) {
+        e = enqueue(sr + 2, w->stage[slot]);
+        if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[slot], cs);
+      }
+    }
   }
   cudaError_t e2 = cudaStreamSynchronize(w->stream);
-  cudaError_t e3 = cudaStreamSynchronize(w->copy_stream);
-  cudaEventDestroy(launched);
+  cudaError_t e3 = cudaStreamSynchronize(cs);
+  cudaEventDestroy(reset);
   if (e == cudaSuccess) e = e2;
   if (e == cudaSuccess) e = e3;
   return cuda_err(e, "sweep/D2H pipeline");
@@ -295,8 +468,7 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
   if (qk_status s = w->ensure(2, size_t(N) * size_t(N) * sizeof(double))) return s;
   double* dX = static_cast<double*>(w->buf[0]);
   cudaStream_t st = w->stream;
-  if (cudaError_t e = cudaMemcpyAsync(dX, h_angles, xb, cudaMemcpyHostToDevice, st))
-    return cuda_err(e, "H2D angles");
+  if (qk_status s = upload(w, dX, h_angles, xb)) return s;
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
@@ -329,10 +501,10 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   char* dPr = static_cast<char*>(w->buf[1]);
   char* dPc = dPr + prb;
   cudaStream_t st = w->stream;
-  cudaError_t e = cudaMemcpyAsync(dXr, h_rows, xrb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dXc, h_cols, xcb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st);
-  if (e != cudaSuccess) return cuda_err(e, "H2D angles");
+  if (qk_status s = upload(w, dXr, h_rows, xrb)) return s;
+  if (qk_status s = upload(w, dXc, h_cols, xcb)) return s;
+  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+    return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
   if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st)) return s;
   if (qk_status s = sweep_and_drain(w, *p, kModeCross, dPr, n_rows, dPc, n_cols,
