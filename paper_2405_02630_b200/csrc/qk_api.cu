@@ -200,18 +200,16 @@ qk_status upload(Workspace* w, void* dst, const void* src, size_t bytes) {
     return cuda_err(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, w->stream), "H2D");
   const size_t chunk = size_t(64) << 20;
   if (qk_status s = w->ensure_stage(chunk)) return s;
-  bool used[2] = {false, false};
   size_t k = 0;
   for (size_t off = 0; off < bytes; off += chunk, ++k) {
     const int slot = int(k & 1);
     const size_t n = std::min(chunk, bytes - off);
-    if (used[slot]) cudaEventSynchronize(w->stage_ev[slot]);
+    cudaEventSynchronize(w->stage_ev[slot]);  // the slot's previous DMA (any call) is done
     copy_pool().copy(w->stage[slot], static_cast<const char*>(src) + off, n);
     cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, w->stage[slot], n,
                                     cudaMemcpyHostToDevice, w->stream);
     if (e != cudaSuccess) return cuda_err(e, "H2D staged");
     cudaEventRecord(w->stage_ev[slot], w->stream);
-    used[slot] = true;
   }
   return QK_OK;
 }

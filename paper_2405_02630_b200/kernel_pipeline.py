@@ -18,8 +18,9 @@ stay on the device.  There is no CPU compute path.
 """
 from __future__ import annotations
 
+import mmap
 from dataclasses import dataclass, field
-from math import ceil
+from math import ceil, prod
 from typing import Any, Iterable
 
 import numpy as np
@@ -156,6 +157,20 @@ def _is_cuda_tensor(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
 
+def host_empty(shape) -> np.ndarray:
+    """Uninitialised float64 host array; large ones are anonymous mappings advised to use
+    transparent huge pages, so the first touch by the copy-out pool faults 2 MB at a time."""
+    nbytes = prod(shape) * 8
+    if nbytes < (64 << 20):
+        return np.empty(shape, dtype=np.float64)
+    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    try:
+        buf.madvise(mmap.MADV_HUGEPAGE)
+    except (AttributeError, OSError):  # pragma: no cover - platform without THP advice
+        pass
+    return np.frombuffer(buf, dtype=np.float64).reshape(shape)
+
+
 def _host_angles(x, width: int) -> np.ndarray:
     a = np.ascontiguousarray(x, dtype=np.float64)
     if a.ndim == 1 and a.size == 0:
@@ -216,7 +231,7 @@ def compute_kernel_matrix(features, cfg, plan=None, workers: int = 1, *,
     if N >= 2 and X.shape[1] != cfg.width:
         raise _width_error(X.shape[1], X.shape[1], cfg.width)
     if out is None:
-        out = np.empty((N, N), dtype=np.float64)
+        out = host_empty((N, N))
     elif out.shape != (N, N) or out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError(f"out must be a C-contiguous float64 array of shape ({N}, {N})")
     if N == 1:
@@ -249,7 +264,7 @@ def compute_cross_kernel(test, train, cfg, plan=None, workers: int = 1, *,
     if Nt and Nr and (T.shape[1] != cfg.width or R.shape[1] != cfg.width):
         raise _width_error(T.shape[1], R.shape[1], cfg.width)
     if out is None:
-        out = np.empty((Nt, Nr), dtype=np.float64)
+        out = host_empty((Nt, Nr))
     elif out.shape != (Nt, Nr) or out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError(f"out must be a C-contiguous float64 array of shape ({Nt}, {Nr})")
     if Nt and Nr:

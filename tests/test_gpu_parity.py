@@ -164,7 +164,7 @@ def test_kernel_job_world1_matches_public_api(rng):
 
 
 def test_pinned_output_pipeline_matches_pageable(rng):
-    n, N = 128, 700
+    n, N = 64, 1300  # 21 tile rows -> 3 super-row panels
     X = rng.uniform(0, 0.2, (N, n))
     cfg = FeatureMapConfig(n)
     pinned = torch.empty((N, N), dtype=torch.float64, pin_memory=True).numpy()

@@ -32,13 +32,15 @@ for rep in range(3):
     compute_cross_kernel(h_te, h_tr, cfg, out=h_Kx); t2 = time.perf_counter()
 out["gram_host_ms"] = 1e3 * (t1 - t)
 out["cross_host_ms"] = 1e3 * (t2 - t1)
-t = time.perf_counter(); compute_kernel_matrix(Atr, cfg); out["gram_host_pageable_ms"] = 1e3 * (time.perf_counter() - t)
+for rep in range(2):
+    t = time.perf_counter(); compute_kernel_matrix(Atr, cfg); out[f"gram_host_default_out_ms_{rep}"] = 1e3 * (time.perf_counter() - t)
+    t = time.perf_counter(); compute_kernel_matrix(Atr, cfg, out=np.empty((10000, 10000))); out[f"gram_host_npempty_out_ms_{rep}"] = 1e3 * (time.perf_counter() - t)
 plan = plan_for(cfg)
 tr = torch.as_tensor(Atr, device="cuda"); te = torch.as_tensor(Ate, device="cuda")
-for rep in range(2):
+for rep in range(3):
     torch.cuda.synchronize(); t = time.perf_counter()
     p = dev.gate_build(plan, tr); K = dev.gram(p); torch.cuda.synchronize(); t1 = time.perf_counter()
     q = dev.gate_build(plan, te); Kx = dev.cross(q, p); torch.cuda.synchronize(); t2 = time.perf_counter()
-out["gram_device_ms"] = 1e3 * (t1 - t)
-out["cross_device_ms"] = 1e3 * (t2 - t1)
+    out[f"gram_device_ms_{rep}"] = 1e3 * (t1 - t)
+    out[f"cross_device_ms_{rep}"] = 1e3 * (t2 - t1)
 print(json.dumps(out))
