@@ -1,0 +1,46 @@
+"""Summarise ncu captures (run here, no GPU): key metrics per kernel launch as CSV/markdown."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__cycles_elapsed.avg.per_second", "sm clock"),
+    ("launch__grid_size", "grid"), ("launch__block_size", "block"),
+    ("launch__registers_per_thread", "regs/thread"),
+    ("launch__shared_mem_per_block_dynamic", "dyn smem/CTA"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("smsp__inst_executed.sum", "warp instr executed"),
+    ("dram__bytes_read.sum", "DRAM read"), ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math/issue"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait/issue"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_sb/issue"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier/issue"),
+    ("smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio", "stall not_selected/issue"),
+]
+
+
+def rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    h, units = r[0], r[1]
+    for v in r[2:]:
+        d = dict(zip(h, v))
+        yield d, dict(zip(h, units))
+
+
+for rep in sys.argv[1:]:
+    for d, u in rows(rep):
+        print(f"### {d.get('Kernel Name', '?')[:90]}  ({rep.split('/')[-1]})")
+        print("| metric | value |\n|---|---|")
+        for k, name in KEYS:
+            if k in d:
+                print(f"| {name} (`{k}`) | {d[k]} {u.get(k, '')} |")
+        print()
