@@ -141,6 +141,20 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
 /* ---- measurement helper: fp64 FMA issue-rate microbenchmark (FLOP/s) ------------- */
 qk_status qk_dfma_peak(double* out_flops_per_s, void* stream);
 
+/* ---- multi-GPU result placement over peer memory (NVLink / NVSwitch) ------------------
+ * Replaces the reference's result collection across workers (engine.py:159-166 pool
+ * gather; SPEC.md:425-434 shard merge; PAPER.md:359-362 MPI/NCCL): rank 0 allocates the
+ * dense kernel matrices with qk_shared_alloc and exports them; every other rank imports the
+ * handle and passes the imported pointer as d_out of qk_gram_tiles / qk_cross_tiles
+ * (QK_OUT_DENSE), so each sweep stores its tiles (and their mirror) straight into rank 0's
+ * matrix — no gather buffer, no unpack.  CUDA IPC; requires peer access between devices. */
+#define QK_IPC_HANDLE_BYTES 64
+qk_status qk_shared_alloc(size_t bytes, void** out_d_ptr);
+qk_status qk_shared_free(void* d_ptr);
+qk_status qk_ipc_export(const void* d_ptr, unsigned char out_handle[QK_IPC_HANDLE_BYTES]);
+qk_status qk_ipc_import(const unsigned char handle[QK_IPC_HANDLE_BYTES], void** out_d_ptr);
+qk_status qk_ipc_close(void* d_ptr);
+
 #ifdef __cplusplus
 }
 #endif

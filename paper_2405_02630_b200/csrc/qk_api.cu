@@ -513,3 +513,48 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
 }
 
 }  // extern "C"
+
+// ---- multi-GPU result placement (CUDA IPC over NVLink / NVSwitch) ------------------------
+extern "C" {
+
+qk_status qk_shared_alloc(size_t bytes, void** out_d_ptr) {
+  if (out_d_ptr == nullptr) return set_error(QK_ERR_VALUE, "NULL output");
+  *out_d_ptr = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaError_t e = cudaMalloc(out_d_ptr, bytes))
+    return set_error(QK_ERR_CAPACITY, std::string("shared allocation of ") +
+                                          std::to_string(bytes) + " bytes failed: " +
+                                          cudaGetErrorString(e));
+  return QK_OK;
+}
+
+qk_status qk_shared_free(void* d_ptr) {
+  if (d_ptr == nullptr) return QK_OK;
+  return cuda_err(cudaFree(d_ptr), "shared free");
+}
+
+qk_status qk_ipc_export(const void* d_ptr, unsigned char out_handle[QK_IPC_HANDLE_BYTES]) {
+  if (d_ptr == nullptr || out_handle == nullptr) return set_error(QK_ERR_VALUE, "NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == QK_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  if (cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)))
+    return cuda_err(e, "cudaIpcGetMemHandle (pointer must come from qk_shared_alloc)");
+  std::memcpy(out_handle, &h, sizeof(h));
+  return QK_OK;
+}
+
+qk_status qk_ipc_import(const unsigned char handle[QK_IPC_HANDLE_BYTES], void** out_d_ptr) {
+  if (handle == nullptr || out_d_ptr == nullptr) return set_error(QK_ERR_VALUE, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  *out_d_ptr = nullptr;
+  return cuda_err(cudaIpcOpenMemHandle(out_d_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                  "cudaIpcOpenMemHandle");
+}
+
+qk_status qk_ipc_close(void* d_ptr) {
+  if (d_ptr == nullptr) return QK_OK;
+  return cuda_err(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
+}
+
+}  // extern "C"

@@ -107,6 +107,21 @@ def cross(rows: Planes, cols: Planes, out: torch.Tensor | None = None, tile_begi
     return out
 
 
+def gram_into(planes: Planes, out_ptr: int, tile_begin: int, tile_end: int) -> None:
+    """Dense Gram tiles [tile_begin, tile_end) stored at a raw device address (e.g. a peer
+    rank's matrix imported over CUDA IPC; row-major N x N)."""
+    _native.check(_native.lib().qk_gram_tiles(planes.plan.handle, planes.ptr(), planes.n,
+                                              tile_begin, tile_end, out_ptr,
+                                              _native.QK_OUT_DENSE, _stream()))
+
+
+def cross_into(rows: Planes, cols: Planes, out_ptr: int, tile_begin: int, tile_end: int) -> None:
+    """Dense cross tiles stored at a raw device address (row-major n_rows x n_cols)."""
+    _native.check(_native.lib().qk_cross_tiles(rows.plan.handle, rows.ptr(), rows.n, cols.ptr(),
+                                               cols.n, tile_begin, tile_end, out_ptr, cols.n,
+                                               _native.QK_OUT_DENSE, _stream()))
+
+
 def unpack_gram(plan: SweepPlan, packed: torch.Tensor, n: int, tile_begin: int, tile_end: int,
                 K: torch.Tensor) -> torch.Tensor:
     _require(packed, "packed", torch.float64)

@@ -1,27 +1,34 @@
-"""Multi-GPU sharding of the kernel-matrix job: one process per GPU, one gather.
+"""Multi-GPU sharding of the kernel-matrix job: one process per GPU.
 
 The reference parallelises over pairs only — a fork pool in code (engine.py:159-166),
 shard-run-then-merge in SPEC, MPI + NCCL across A100s in the paper
 (PAPER.md:359-362).  Here the unit is the sweep tile: the job's linearised tile list (train
 Gram upper-triangle tiles, then test x train cross tiles) is split into contiguous equal
 ranges (SPEC's contiguous ceil(P/W) rule at tile granularity; every tile costs the same, so
-equal counts are balanced).  Each rank builds the gate planes of every sample (cheap),
-sweeps its range into a packed buffer padded to the common range length, and ONE
-``gather`` over NCCL (NVLink / NVSwitch) brings the packed tiles to rank 0, which scatters
-them into the dense matrices with the unpack kernel.  World size 1 writes the dense
-matrices directly.
+equal counts are balanced).  Each rank builds the gate planes of every sample (cheap) and
+sweeps its range.  Two ways to land the results on rank 0:
 
-The partition / gather / placement logic is device-agnostic (tested with gloo on CPU);
-the sweeps and unpacks are the CUDA kernels.
+* ``placement="p2p"`` (default): rank 0 allocates the dense matrices and exports them over
+  CUDA IPC; every rank's sweep kernel stores its tiles — and their mirror — straight into
+  rank 0's memory over NVLink / NVSwitch while it computes.  Completion is one barrier.  No
+  gather buffer, no unpack: the collective is fused into the compute kernel's epilogue.
+* ``placement="gather"``: packed tiles padded to the common range length, one ``gather`` to
+  rank 0 (NCCL), then the unpack kernel.  For fabrics without peer access.
+
+World size 1 writes the dense matrices directly.  The partition / placement logic is
+device-agnostic (tested with gloo on CPU); the p2p path is tested with two processes sharing
+one GPU (CUDA IPC works within a device), the sweeps/unpacks by the GPU parity tests.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from math import ceil
 
 import torch
 import torch.distributed as dist
 
+from . import _native
 from .kernel_pipeline import shard_range
 from .planner import SweepPlan
 
@@ -80,21 +87,75 @@ def layout_for(plan: SweepPlan, n_train: int, n_test: int, world: int) -> JobLay
 
 
 def gather_packed(local: torch.Tensor, layout: JobLayout, group=None) -> list | None:
-    """Gather every rank's padded packed buffer to rank 0 (one collective)."""
+    """Gather every rank's padded packed buffer to rank 0 (one collective).  gloo has no
+    CUDA gather, so a gloo group moves the buffers through host memory."""
     rank = dist.get_rank(group)
     if layout.world == 1:
         return [local]
-    bufs = [torch.empty_like(local) for _ in range(layout.world)] if rank == 0 else None
-    dist.gather(local, bufs, dst=0, group=group)
+    src = local
+    if dist.get_backend(group) == "gloo" and local.is_cuda:
+        src = local.cpu()
+    bufs = [torch.empty_like(src) for _ in range(layout.world)] if rank == 0 else None
+    dist.gather(src, bufs, dst=0, group=group)
+    if bufs is not None and local.is_cuda:
+        bufs = [b.to(local.device) for b in bufs]
     return bufs
+
+
+class SharedMatrix:
+    """Dense row-major fp64 matrix in device memory that peer processes can store into.
+
+    The owner allocates it with ``qk_shared_alloc`` and exports a CUDA IPC handle; peers
+    import the handle and get a device address of the same memory (over NVLink when the
+    owner is another GPU).  The owner's view is also a torch tensor (``tensor``)."""
+
+    def __init__(self, rows: int, cols: int, handle: bytes | None = None):
+        self.rows, self.cols = int(rows), int(cols)
+        self.owner = handle is None
+        lib = _native.lib()
+        p = ctypes.c_void_p()
+        if self.owner:
+            _native.check(lib.qk_shared_alloc(max(1, self.rows * self.cols) * 8,
+                                              ctypes.byref(p)))
+        else:
+            _native.check(lib.qk_ipc_import(handle, ctypes.byref(p)))
+        self.ptr = int(p.value)
+        self.__cuda_array_interface__ = {"shape": (self.rows, self.cols), "typestr": "<f8",
+                                         "data": (self.ptr, False), "version": 3,
+                                         "strides": None}
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _native.check(_native.lib().qk_ipc_export(self.ptr, buf))
+        return buf.raw
+
+    def tensor(self) -> torch.Tensor:
+        assert self.owner, "only the owner views the matrix as a tensor"
+        return torch.as_tensor(self, device=torch.device("cuda", torch.cuda.current_device()))
+
+    def close(self) -> None:
+        if self.ptr and _native._lib is not None:
+            lib = _native._lib
+            (lib.qk_shared_free if self.owner else lib.qk_ipc_close)(self.ptr)
+        self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
 
 
 class KernelJob:
     """Train Gram (+ optional test x train cross block) over a process group."""
 
-    def __init__(self, plan: SweepPlan, n_train: int, n_test: int = 0, group=None):
+    def __init__(self, plan: SweepPlan, n_train: int, n_test: int = 0, group=None,
+                 placement: str = "p2p"):
+        if placement not in ("p2p", "gather"):
+            raise ValueError(f"unknown placement {placement!r}")
         self.plan = plan
         self.group = group
+        self.placement = placement
         if dist.is_available() and dist.is_initialized():
             self.rank = dist.get_rank(group)
             self.world = dist.get_world_size(group)
@@ -104,26 +165,67 @@ class KernelJob:
         self.packed = None
         self.K_train = None
         self.K_cross = None
+        self._shared = None
 
-    def run(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None):
-        """Returns (K_train, K_cross) on rank 0 (device tensors), (None, None) elsewhere."""
+    # ---- world size 1 ----------------------------------------------------------------
+    def _run_local(self, p_train, p_test, devc):
         from . import device as dev
 
         lay = self.layout
-        p_train = dev.gate_build(self.plan, train_angles)
-        p_test = dev.gate_build(self.plan, test_angles) if lay.n_test else None
-        devc = train_angles.device
-        if self.world == 1:
-            if self.K_train is None:
-                self.K_train = torch.empty((lay.n_train, lay.n_train), dtype=torch.float64,
-                                           device=devc)
-                if lay.n_test:
-                    self.K_cross = torch.empty((lay.n_test, lay.n_train), dtype=torch.float64,
-                                               device=devc)
-            dev.gram(p_train, out=self.K_train)
+        if self.K_train is None:
+            self.K_train = torch.empty((lay.n_train, lay.n_train), dtype=torch.float64,
+                                       device=devc)
             if lay.n_test:
-                dev.cross(p_test, p_train, out=self.K_cross)
-            return self.K_train, self.K_cross
+                self.K_cross = torch.empty((lay.n_test, lay.n_train), dtype=torch.float64,
+                                           device=devc)
+        dev.gram(p_train, out=self.K_train)
+        if lay.n_test:
+            dev.cross(p_test, p_train, out=self.K_cross)
+        return self.K_train, self.K_cross
+
+    # ---- p2p placement: sweeps store into rank 0's matrices ----------------------------
+    def _setup_shared(self):
+        lay = self.layout
+        if self.rank == 0:
+            mats = [SharedMatrix(lay.n_train, lay.n_train)]
+            if lay.n_test:
+                mats.append(SharedMatrix(lay.n_test, lay.n_train))
+            handles = [m.export() for m in mats]
+        else:
+            mats, handles = None, None
+        box = [handles]
+        dist.broadcast_object_list(box, src=0, group=self.group)
+        if self.rank != 0:
+            shapes = [(lay.n_train, lay.n_train), (lay.n_test, lay.n_train)]
+            mats = [SharedMatrix(r, c, handle=h) for (r, c), h in zip(shapes, box[0])]
+        self._shared = mats
+        if self.rank == 0:
+            self.K_train = mats[0].tensor()
+            self.K_cross = mats[1].tensor() if lay.n_test else None
+
+    def _run_p2p(self, p_train, p_test):
+        from . import device as dev
+
+        if self._shared is None:
+            self._setup_shared()
+        lay = self.layout
+        for seg in lay.segments(self.rank):
+            if seg.kind == "gram":
+                dev.gram_into(p_train, self._shared[0].ptr, seg.tile_begin, seg.tile_end)
+            else:
+                dev.cross_into(p_test, p_train, self._shared[1].ptr, seg.tile_begin,
+                               seg.tile_end)
+        torch.cuda.current_stream().synchronize()  # this rank's stores have landed
+        dist.barrier(group=self.group)
+        if self.rank != 0:
+            return None, None
+        return self.K_train, self.K_cross
+
+    # ---- gather placement --------------------------------------------------------------
+    def _run_gather(self, p_train, p_test, devc):
+        from . import device as dev
+
+        lay = self.layout
         if self.packed is None:
             self.packed = torch.empty(max(lay.range_len, 1) * lay.tile_elems,
                                       dtype=torch.float64, device=devc)
@@ -156,3 +258,21 @@ class KernelJob:
                     dev.unpack_cross(self.plan, view, lay.n_test, lay.n_train, seg.tile_begin,
                                      seg.tile_end, self.K_cross)
         return self.K_train, self.K_cross
+
+    def run(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None):
+        """Returns (K_train, K_cross) on rank 0 (device tensors), (None, None) elsewhere."""
+        from . import device as dev
+
+        p_train = dev.gate_build(self.plan, train_angles)
+        p_test = dev.gate_build(self.plan, test_angles) if self.layout.n_test else None
+        if self.world == 1:
+            return self._run_local(p_train, p_test, train_angles.device)
+        if self.placement == "p2p":
+            return self._run_p2p(p_train, p_test)
+        return self._run_gather(p_train, p_test, train_angles.device)
+
+    def close(self) -> None:
+        if self._shared:
+            for m in self._shared:
+                m.close()
+            self._shared = None

@@ -1,0 +1,78 @@
+"""The multi-GPU job path with two real processes.  Only one GPU is available to the test
+run, so both ranks share cuda:0 (CUDA IPC between processes works within a device) and the
+process group is gloo; on an 8-GPU box the same code runs one rank per GPU over NCCL with
+the IPC stores going over NVLink.  Both placements must reproduce the single-process
+matrices bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+N_TRAIN, N_TEST, WIDTH = 333, 71, 40
+
+
+def _data():
+    rng = np.random.default_rng(77)
+    centre = rng.uniform(0, np.pi, WIDTH)
+    return (centre + rng.normal(0, 0.1, (N_TRAIN, WIDTH)),
+            centre + rng.normal(0, 0.1, (N_TEST, WIDTH)))
+
+
+def worker(rank, world, port, placement, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2405_02630_b200 import (FeatureMapConfig, SweepPlan, compute_cross_kernel,
+                                           compute_kernel_matrix)
+        from paper_2405_02630_b200.distributed import KernelJob
+
+        Xtr, Xte = _data()
+        plan = SweepPlan(WIDTH, 2)
+        job = KernelJob(plan, N_TRAIN, N_TEST, placement=placement)
+        for _ in range(2):  # the second run reuses the shared matrices / buffers
+            K, Kx = job.run(torch.as_tensor(Xtr, device="cuda"),
+                            torch.as_tensor(Xte, device="cuda"))
+        if rank == 0:
+            cfg = FeatureMapConfig(WIDTH)
+            ok = (np.array_equal(K.cpu().numpy(), compute_kernel_matrix(Xtr, cfg).entries),
+                  np.array_equal(Kx.cpu().numpy(), compute_cross_kernel(Xte, Xtr, cfg).entries))
+            q.put(ok)
+        dist.barrier()
+        job.close()
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover - surfaced through the queue
+        q.put(repr(exc))
+        raise
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("placement", ["p2p", "gather"])
+def test_two_rank_job_matches_single_process(placement):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=worker, args=(r, 2, port, placement, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=500)
+    for p in procs:
+        p.join(timeout=120)
+    assert res == (True, True), res
+    assert all(p.exitcode == 0 for p in procs)
