@@ -325,3 +325,41 @@ def _compute_cross_kernel_device(test, train, cfg, sp, convention, dataset_id) -
         cands = ([bt * Nr] if bt is not None else []) + ([br] if br is not None else [])
         raise RebindError(f"operand set {min(cands)}: feature angles must be finite")
     return KernelMatrix(Nt, Nr, K, convention, _metadata(cfg, sp, dataset_id, "cross"))
+
+
+# ---------------------------------------------------------------------------------------
+# shard-run-then-merge (CLI `--shard k/W`)
+# ---------------------------------------------------------------------------------------
+def compute_kernel_shard(features, cfg, shard: int, n_shards: int, *, test=None,
+                         convention: str = "probability"):
+    """Values of shard k (0-based) of W: the contiguous ceil(P/W) range of the row-major pair
+    enumeration (strict upper triangle of the train Gram, or the test x train rectangle when
+    ``test`` is given).  Returns ``(pair_range, values)``; merging every shard's partial
+    (container.merge_partials) reproduces compute_kernel_matrix / compute_cross_kernel bit
+    for bit — the pair-list kernel runs the sweep's exact arithmetic."""
+    import torch
+
+    from . import device as dev
+    from .container import enumeration_pairs, shard_pair_range
+
+    cfg = as_config(cfg)
+    convention = check_convention(convention)
+    sp = plan_for(cfg, convention)
+    X = _host_angles(features, cfg.width) if not _is_cuda_tensor(features) else features
+    T = None if test is None else (_host_angles(test, cfg.width) if not _is_cuda_tensor(test)
+                                   else test)
+    symmetric = T is None
+    n_a = (X.shape[0] if symmetric else T.shape[0])
+    n_b = X.shape[0]
+    lo, hi = shard_pair_range(n_a, n_b, symmetric, shard, n_shards)
+    if hi <= lo:
+        return (lo, hi), np.empty(0)
+    pairs = torch.as_tensor(enumeration_pairs(n_a, n_b, symmetric, lo, hi), device="cuda")
+    px = dev.gate_build(sp, dev.angles_to_device(X))
+    pa = px if symmetric else dev.gate_build(sp, dev.angles_to_device(T))
+    amp = dev.pair_amplitudes(pa, px, pairs)
+    vals = amp.abs() if convention == "magnitude" else amp * amp
+    bad = [b for b in (px.bad_sample(), None if symmetric else pa.bad_sample()) if b is not None]
+    if bad:
+        raise RebindError("feature angles must be finite")
+    return (lo, hi), vals.cpu().numpy()

@@ -215,3 +215,24 @@ def test_svc_predictions_identical(rng):
     clf = OneVsRestClassifier(SVC(kernel="precomputed", C=1.0)).fit(K, ytr)
     clf_r = OneVsRestClassifier(SVC(kernel="precomputed", C=1.0)).fit(Kr, ytr)
     assert np.array_equal(clf.predict(Kx), clf_r.predict(Kxr))
+
+
+def test_shard_run_then_merge_equals_full_matrix(tmp_path, rng):
+    """`--shard k/W` partials merged == the unsharded matrix, bit for bit."""
+    from paper_2405_02630_b200.container import merge_partials, save_partial
+    from paper_2405_02630_b200.kernel_pipeline import compute_kernel_shard
+
+    n, N = 50, 137
+    X = rng.uniform(0, 0.4, (N, n))
+    T = rng.uniform(0, 0.4, (23, n))
+    cfg = FeatureMapConfig(n)
+    for test, full in [(None, compute_kernel_matrix(X, cfg).entries),
+                       (T, compute_cross_kernel(T, X, cfg).entries)]:
+        paths = []
+        for k in range(3):
+            rng_k, vals = compute_kernel_shard(X, cfg, k, 3, test=test)
+            p = tmp_path / f"{'g' if test is None else 'x'}{k}.qkk"
+            rows = N if test is None else len(T)
+            save_partial(p, vals, rng_k, rows, N, test is None)
+            paths.append(p)
+        assert np.array_equal(merge_partials(paths).entries, full)
