@@ -401,9 +401,11 @@ qk_status sweep_and_drain(Workspace* w, const Plan& p, int mode, const void* d_r
   auto enqueue = [&](int64_t sr, void* dst) -> cudaError_t {
     if (d_prog != nullptr) {
       const int64_t r0 = sr * kGroup, r1 = std::min<int64_t>(r0 + kGroup, nbr);
-      const uint32_t expect = uint32_t(mode == kModeGram
-                                           ? upper_row_offset(r1, nbr) - upper_row_offset(r0, nbr)
-                                           : (r1 - r0) * nbc);
+      const uint32_t unit = p.layers >= 3 ? 16u : 1u;  // L >= 3 counts 16 sub-tiles per tile
+      const uint32_t expect = unit * uint32_t(mode == kModeGram
+                                                  ? upper_row_offset(r1, nbr) -
+                                                        upper_row_offset(r0, nbr)
+                                                  : (r1 - r0) * nbc);
       if (wait(cs, reinterpret_cast<uintptr_t>(d_prog + sr), expect, 0x0) != 0)
         return cudaErrorNotSupported;
     }

@@ -48,11 +48,11 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   if (layers < 1) return set_error(QK_ERR_VALUE, "layers must be >= 1");
   if (convention != QK_PROBABILITY && convention != QK_MAGNITUDE)
     return set_error(QK_ERR_VALUE, "unknown kernel convention " + std::to_string(convention));
-  if (layers > 2)
+  if (layers > 3)
     return set_error(QK_ERR_CAPACITY,
                      "layers=" + std::to_string(layers) +
                          " needs a bond-" + std::to_string(1 << (2 * (layers - 1))) +
-                         " transfer state; the sm_100a sweep implements layers 1 and 2");
+                         " transfer state; the sm_100a sweep implements layers 1, 2 and 3");
 
   qk_plan* h = new (std::nothrow) qk_plan();
   if (h == nullptr) return set_error(QK_ERR_CAPACITY, "out of host memory");
@@ -77,7 +77,7 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   in.width = width;
   in.layers = layers;
   in.convention = convention;
-  in.bond = layers == 1 ? 1 : 4;
+  in.bond = 1 << (2 * (layers - 1));
   in.tile_edge = kTile;
   in.chunk = kChunk;
   in.width_padded = p.width_padded;
@@ -89,11 +89,18 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
     in.flops_per_entry = 24 * n + 3;
     in.algorithmic_flops_per_entry = 34 * n + 4;
     in.reference_cmacs_per_entry = n >= 8 ? 1056 * n - 3912 : 0;
-  } else {
+  } else if (layers == 1) {
     // per qubit per pair: DMUL + DFMA + DMUL
     in.dp_instr_per_entry = 3 * n;
     in.flops_per_entry = 4 * n;
     in.algorithmic_flops_per_entry = 4 * n;
+    in.reference_cmacs_per_entry = 0;
+  } else {
+    // L = 3 per qubit per pair: two 4x4 site matrices (32 DMUL), F_i^T V and (.)F_j
+    // (2 x (16 DMUL + 48 DFMA)), RY(delta) (2 DMUL + 2 DFMA) and the mask (16 DMUL)
+    in.dp_instr_per_entry = 180 * n + 15;
+    in.flops_per_entry = 278 * n + 15;
+    in.algorithmic_flops_per_entry = 278 * n + 15;
     in.reference_cmacs_per_entry = 0;
   }
   *out_plan = h;

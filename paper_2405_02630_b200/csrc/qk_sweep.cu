@@ -147,6 +147,83 @@ __device__ __forceinline__ void bond1_step(Bond1& s, double2 vi, double2 vj) {
   s.v *= fma(vi.y, vj.y, vi.x * vj.x);  // cos((x_j - x_i)/2) from half-angle planes
 }
 
+// L >= 3: amp = <phi_{L-1}(x_i)| R(x_j - x_i) |phi_{L-1}(x_j)>, phi_m = (C R)^m |0> is an MPS
+// of bond D = 2^m whose site matrix is F(x)[a][b] = prod_k RY(x)[a_k ^ b_k][b_{k-1}] (level-k
+// bits, b_0 = 0); the pair state V is D x D and one qubit is V <- (F_i^T V F_j) o RY(delta)
+// on the top-level bits.  Half-angle planes (c, s).  |V| <= 1: no rescaling.
+template <int M>
+struct BondG {
+  static constexpr int D = 1 << M;
+  double v[D][D];
+};
+
+template <int M>
+__device__ __forceinline__ void site_matrix(double (&F)[1 << M][1 << M], double c, double s) {
+  constexpr int D = 1 << M;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      double f = 1.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const int r = ((a >> k) ^ (b >> k)) & 1;            // RY row: a_k ^ b_k
+        const int col = k == 0 ? 0 : ((b >> (k - 1)) & 1);  // RY column: b_{k-1}
+        const double e = col == 0 ? (r ? s : c) : (r ? c : -s);
+        f = k == 0 ? e : f * e;
+      }
+      F[a][b] = f;
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void bondg_init(BondG<M>& s) {
+#pragma unroll
+  for (int a = 0; a < BondG<M>::D; ++a)
+#pragma unroll
+    for (int b = 0; b < BondG<M>::D; ++b) s.v[a][b] = (a == 0 && b == 0) ? 1.0 : 0.0;
+}
+
+template <int M>
+__device__ __forceinline__ void bondg_step(BondG<M>& s, double2 vi, double2 vj) {
+  constexpr int D = 1 << M;
+  double Fi[D][D], Fj[D][D], W[D][D];
+  site_matrix<M>(Fi, vi.x, vi.y);
+  site_matrix<M>(Fj, vj.x, vj.y);
+#pragma unroll
+  for (int b = 0; b < D; ++b)  // W = Fi^T V
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double w = Fi[0][b] * s.v[0][a];
+#pragma unroll
+      for (int k = 1; k < D; ++k) w = fma(Fi[k][b], s.v[k][a], w);
+      W[b][a] = w;
+    }
+  const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
+  const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
+#pragma unroll
+  for (int b = 0; b < D; ++b)  // V = (W Fj) o RY(delta)[top bits]
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double v = W[b][0] * Fj[0][c];
+#pragma unroll
+      for (int k = 1; k < D; ++k) v = fma(W[b][k], Fj[k][c], v);
+      const int tb = (b >> (M - 1)) & 1, tc = (c >> (M - 1)) & 1;
+      const double m = tb == tc ? cd : (tb ? sd : -sd);
+      s.v[b][c] = v * m;
+    }
+}
+
+template <int M>
+__device__ __forceinline__ double bondg_amp(const BondG<M>& s) {
+  double acc = 0.0;
+#pragma unroll
+  for (int a = 0; a < BondG<M>::D; ++a)
+#pragma unroll
+    for (int b = 0; b < BondG<M>::D; ++b) acc += s.v[a][b];
+  return acc;
+}
+
 template <int LAYERS>
 struct BondT;
 template <>
@@ -157,14 +234,22 @@ template <>
 struct BondT<2> {
   using type = Bond4;
 };
+template <>
+struct BondT<3> {
+  using type = BondG<2>;
+};
 
 template <int LAYERS>
 __device__ __forceinline__ void st_init(typename BondT<LAYERS>::type& s) {
-  if constexpr (LAYERS == 2) bond4_init(s); else bond1_init(s);
+  if constexpr (LAYERS == 2) bond4_init(s);
+  else if constexpr (LAYERS == 1) bond1_init(s);
+  else bondg_init<LAYERS - 1>(s);
 }
 template <int LAYERS>
 __device__ __forceinline__ void st_step(typename BondT<LAYERS>::type& s, double2 vi, double2 vj) {
-  if constexpr (LAYERS == 2) bond4_step(s, vi, vj); else bond1_step(s, vi, vj);
+  if constexpr (LAYERS == 2) bond4_step(s, vi, vj);
+  else if constexpr (LAYERS == 1) bond1_step(s, vi, vj);
+  else bondg_step<LAYERS - 1>(s, vi, vj);
 }
 template <int LAYERS>
 __device__ __forceinline__ void st_rescale(typename BondT<LAYERS>::type& s) {
@@ -172,7 +257,9 @@ __device__ __forceinline__ void st_rescale(typename BondT<LAYERS>::type& s) {
 }
 template <int LAYERS>
 __device__ __forceinline__ double st_amp(const typename BondT<LAYERS>::type& s, double fs) {
-  if constexpr (LAYERS == 2) return bond4_amp(s, fs); else return s.v;
+  if constexpr (LAYERS == 2) return bond4_amp(s, fs);
+  else if constexpr (LAYERS == 1) return s.v;
+  else return bondg_amp<LAYERS - 1>(s);
 }
 
 __device__ __forceinline__ double kernel_value(double amp, int convention) {
@@ -225,7 +312,7 @@ __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows,
 }
 
 // ------------------------------------------------------------------------------------------
-// Gate build: angles -> planes[block][q][t] = (cos x, sin x)  (L = 2)  or  half angles (L = 1)
+// Gate build: angles -> planes[block][q][t] = (cos x, sin x)  (L = 2)  or  half angles (L != 2)
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gate_build_kernel(const double* __restrict__ X,
                                                          int64_t n_samples, int64_t ld,
@@ -434,6 +521,58 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
 }
 
 // ------------------------------------------------------------------------------------------
+// L >= 3 tiles: the bond-16 state (16 doubles) does not fit a register micro-tile, so each
+// thread carries ONE pair; a 64x64 tile is 16 work items of 16x16 pairs spread over the
+// grid.  Planes are read through L1/L2 (the step is ~180 FP64 instructions per 32 B loaded).
+// ------------------------------------------------------------------------------------------
+template <int LAYERS, int MODE, int OUT>
+__global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
+  using St = typename BondT<LAYERS>::type;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t items = a.n_tiles * 16;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t g = a.tile_begin + it / 16;
+    const int sub = int(it % 16);
+    int64_t bi, bj;
+    if (MODE == kModeGram) {
+      decode_upper(g, a.nb_rows, bi, bj);
+    } else {
+      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+    }
+    const int il = (sub / 4) * 16 + ty, jl = (sub % 4) * 16 + tx;
+    const double2* pi = a.rows + bi * int64_t(a.n_pad) * kTile + il;
+    const double2* pj = a.cols + bj * int64_t(a.n_pad) * kTile + jl;
+    St st;
+    st_init<LAYERS>(st);
+    for (int q = 0; q < a.n_pad; ++q)
+      st_step<LAYERS>(st, __ldg(pi + int64_t(q) * kTile), __ldg(pj + int64_t(q) * kTile));
+    const double v = kernel_value(st_amp<LAYERS>(st, a.final_scale), a.convention);
+    if (OUT == QK_OUT_PACKED) {
+      a.out[(g - a.tile_begin) * int64_t(kTile * kTile) + il * kTile + jl] = v;
+    } else {
+      const int64_t i = bi * kTile + il, j = bj * kTile + jl;
+      if (MODE == kModeGram) {
+        if (i < a.n_rows && j < a.n_rows) {
+          if (i < j) {
+            a.out[i * a.ld_out + j] = v;
+            a.out[j * a.ld_out + i] = v;
+          } else if (i == j) {
+            a.out[i * a.ld_out + i] = 1.0;
+          }
+        }
+      } else if (i < a.n_rows && j < a.n_cols) {
+        a.out[i * a.ld_out + j] = v;
+      }
+    }
+    if (a.progress != nullptr) {
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(a.progress + bi / kGroup, 1u);  // 16 per tile
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Pair-list kernel: one pair per thread, planes read straight from global/L2.
 // ------------------------------------------------------------------------------------------
 template <int LAYERS>
@@ -541,7 +680,7 @@ qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, in
   if (n == 0) return QK_OK;
   dim3 grid(unsigned(blocks_for(n)), unsigned((p.width_padded + 31) / 32));
   gate_build_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      d_angles, n, ld, p.width, p.width_padded, p.front_pad, p.layers == 1 ? 1 : 0,
+      d_angles, n, ld, p.width, p.width_padded, p.front_pad, p.layers == 2 ? 0 : 1,
       static_cast<double2*>(d_planes), reinterpret_cast<unsigned long long*>(d_bad));
   return cuda_status(cudaGetLastError(), "gate_build launch");
 }
@@ -581,6 +720,20 @@ static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   return launch_sweep_ri<LAYERS, MODE, OUT, 4>(a, st);
 }
 
+template <int LAYERS, int MODE, int OUT>
+static qk_status launch_general(const SweepArgs& a, cudaStream_t st) {
+  auto kern = sweep_general_kernel<LAYERS, MODE, OUT>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+  if (e != cudaSuccess) return cuda_status(e, "general sweep occupancy");
+  const int sms = sm_count();
+  if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
+  int64_t grid = int64_t(sms) * (per_sm < 1 ? 1 : per_sm);
+  if (grid > a.n_tiles * 16) grid = a.n_tiles * 16;
+  kern<<<unsigned(grid), 256, 0, st>>>(a);
+  return cuda_status(cudaGetLastError(), "general sweep launch");
+}
+
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
@@ -611,11 +764,18 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
     return packed ? launch_sweep_t<2, kModeCross, QK_OUT_PACKED>(a, st)
                   : launch_sweep_t<2, kModeCross, QK_OUT_DENSE>(a, st);
   }
+  if (p.layers == 1) {
+    if (mode == kModeGram)
+      return packed ? launch_sweep_t<1, kModeGram, QK_OUT_PACKED>(a, st)
+                    : launch_sweep_t<1, kModeGram, QK_OUT_DENSE>(a, st);
+    return packed ? launch_sweep_t<1, kModeCross, QK_OUT_PACKED>(a, st)
+                  : launch_sweep_t<1, kModeCross, QK_OUT_DENSE>(a, st);
+  }
   if (mode == kModeGram)
-    return packed ? launch_sweep_t<1, kModeGram, QK_OUT_PACKED>(a, st)
-                  : launch_sweep_t<1, kModeGram, QK_OUT_DENSE>(a, st);
-  return packed ? launch_sweep_t<1, kModeCross, QK_OUT_PACKED>(a, st)
-                : launch_sweep_t<1, kModeCross, QK_OUT_DENSE>(a, st);
+    return packed ? launch_general<3, kModeGram, QK_OUT_PACKED>(a, st)
+                  : launch_general<3, kModeGram, QK_OUT_DENSE>(a, st);
+  return packed ? launch_general<3, kModeCross, QK_OUT_PACKED>(a, st)
+                : launch_general<3, kModeCross, QK_OUT_DENSE>(a, st);
 }
 
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
@@ -642,6 +802,10 @@ qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* 
   const int nchunks = p.width_padded / kChunk;
   if (p.layers == 2)
     pairs_kernel<2><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
+                                          static_cast<const double2*>(d_b), n_b, d_pairs,
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
+  else if (p.layers == 3)
+    pairs_kernel<3><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
                                           n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
   else
