@@ -3,7 +3,9 @@
 Workload (BASELINE.json configs[3], the config the 1/2/4/8-GPU metric is quoted on; it fits one
 GPU): MNIST-shaped synthetic data, 784 qubits, L = 2, train Gram 10000 x 10000 (49,995,000
 strict-upper entries; diagonal injected) + test-versus-train cross 2000 x 10000 (20,000,000
-entries).  One step = gate build + pair sweeps + (N > 1) NCCL gather + unpack of the whole job.
+entries).  One step = gate build + pair sweeps of the whole job; for N > 1 the tile list is
+split into equal contiguous ranges and every rank's sweep stores its tiles straight into rank
+0's matrices over NVLink (CUDA IPC), closed by one barrier (distributed.py).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -210,9 +212,17 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # QK_BENCH_SHARED_GPU=1 (testing the multi-rank code path on a one-GPU box): every rank
+    # on cuda:0 with a gloo process group.  Never set for a measurement.
+    shared_gpu = os.environ.get("QK_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2405_02630_b200 import (FeatureMapConfig, compute_cross_kernel,
                                        compute_kernel_matrix, plan_for)
     from paper_2405_02630_b200 import device as qdev
@@ -251,6 +261,12 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def allreduce_scalar(v, op):
+        dev_ = "cpu" if dist.get_backend() == "gloo" else "cuda"
+        t = torch.tensor([float(v)], device=dev_, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
     for _ in range(args.warmup):
         job.run(tr, te)
     barrier()
@@ -269,16 +285,14 @@ def run_ours(args):
     recording[0] = False
     elapsed = t0.elapsed_time(t1) / 1e3
     if world > 1:
-        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
+        elapsed = allreduce_scalar(elapsed, dist.ReduceOp.MAX)
     barrier()
     clk = clocks.stop() if rank == 0 else None
     qdev.gram, qdev.cross = orig_gram, orig_cross
 
     sweep_s = sum(a.elapsed_time(b) for a, b in sweep_events) / 1e3
     launches_per_step = 2 + len(sweep_events) // max(1, args.steps)
-    if world > 1 and rank == 0:
+    if world > 1 and rank == 0 and job.placement == "gather":  # unpack launches
         launches_per_step += sum(len(job.layout.segments(r)) for r in range(world))
     value = entries * args.steps / elapsed
 
@@ -359,24 +373,23 @@ def run_ours(args):
         barrier()
         e_el = time.perf_counter() - w0
         if world > 1:
-            tt = torch.tensor([e_el], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_el = float(tt.item())
+            e_el = allreduce_scalar(e_el, dist.ReduceOp.MAX)
         e2e = {"value": entries * args.e2e_steps / e_el, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d * (world if world > 1 else 1)),
                "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                "ms_per_step": 1e3 * e_el / args.e2e_steps,
                "api": "compute_kernel_matrix + compute_cross_kernel (C-ABI host pipeline)"
-               if world == 1 else "KernelJob over NCCL + pinned H2D/D2H"}
+               if world == 1 else "KernelJob (sweeps store into rank 0 over NVLink) + pinned "
+                                  "H2D/D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_run(Atr, Ate, args.cpu_seconds)
         cpu.pop("seconds", None)
 
-    launches_total = torch.tensor([launches_per_step * args.steps], device="cuda")
+    launches_total = launches_per_step * args.steps
     if world > 1:
-        dist.all_reduce(launches_total)
+        launches_total = allreduce_scalar(launches_total, dist.ReduceOp.SUM)
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup,
@@ -385,7 +398,7 @@ def run_ours(args):
                "config": dict(WORKLOAD, parallelism=f"tile-sharded x{world}",
                               entries_per_step=entries),
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-               "gpu_launches": int(launches_total.item()),
+               "gpu_launches": int(launches_total),
                "gpu": props.name, "plan": info}
         print(json.dumps(out), flush=True)
     if world > 1:
