@@ -109,19 +109,50 @@ __device__ __forceinline__ void bond4_init(Bond4& s) {
 }
 
 // 4 DMUL + 4 DADD + 8 DFMA per pair-qubit.  Six of the DFMAs read three distinct registers;
-// the FP64 pipe issues those at ~2/3 rate unless an operand hits the reuse cache (register-file
-// read bandwidth; measured with tools/rfbench.cu: 0.33 vs 0.49 warp-instr/clk/SMSP).  The
-// alternatives that distribute the sums into FMA chains (4 DMUL + 12 DFMA) have more
-// three-source DFMAs and measured 5-9% slower.
+// the FP64 pipe issues those at ~2/3 rate unless an operand hits the operand-reuse cache
+// (register-file read bandwidth; tools/rfbench.cu: 0.33 vs 0.49 warp-instr/clk/SMSP), so the
+// operand order is chosen to let pairs of three-source DFMAs share a register in one slot.
+// QK_STEPV selects among the measured orderings (config-4 bench, RI = 2 / RI = 4, G entries/s):
+//   1: c/d plain, T+ and T- shared in slot B            1.209 / 1.201
+//   2: + c and d share b_i in slot A          (default)  1.220 / 1.202
+//   3: c and d share b_j in slot A                        1.210 / 1.202
+//   4: T+/T- shared in slot A                             1.211 / 1.202
+//   5: no sharing (first version)                         1.195 / 1.196
+//   6: 2 + 4                                              1.220 / 1.203
+// Distributing the sums into FMA chains (4 DMUL + 12 DFMA) adds three-source DFMAs and
+// measured 5-9 % slower.
+#ifndef QK_STEPV
+#define QK_STEPV 2
+#endif
 __device__ __forceinline__ void bond4_step(Bond4& s, double2 vi, double2 vj) {
   const double ai = vi.x, bi = vi.y, aj = vj.x, bj = vj.y;
+#if QK_STEPV == 1 || QK_STEPV == 4 || QK_STEPV == 5
   const double c = fma(bi, bj, ai * aj);     // cos(x_j - x_i)
   const double d = fma(ai, bj, -(bi * aj));  // sin(x_j - x_i)
+#elif QK_STEPV == 2 || QK_STEPV == 6
+  const double c = fma(bi, bj, ai * aj);
+  const double d = fma(-bi, aj, ai * bj);  // shares b_i (slot A) with c
+#else
+  const double c = fma(bj, bi, aj * ai);
+  const double d = fma(bj, ai, -(aj * bi));  // shares b_j (slot A) with c
+#endif
   const double s1 = bi + bj, d2 = bi - bj, s2 = ai + aj, d1 = aj - ai;
+#if QK_STEPV == 4 || QK_STEPV == 6
+  const double nsp = fma(s.tp, s1, fma(s.sp, c, s.sp));
+  const double ntm = fma(s.tp, -d, s.sp * d1);  // shares T+ (slot A) with nsp
+  const double nsm = fma(s.tm, d, s.sm * s2);
+  const double ntp = fma(s.tm, d2, fma(s.sm, c, -s.sm));  // shares T- (slot A) with nsm
+#elif QK_STEPV == 5
   const double nsp = fma(s1, s.tp, fma(c, s.sp, s.sp));
   const double ntm = fma(d1, s.sp, -(d * s.tp));
   const double nsm = fma(d, s.tm, s2 * s.sm);
   const double ntp = fma(d2, s.tm, fma(c, s.sm, -s.sm));
+#else
+  const double nsp = fma(s1, s.tp, fma(c, s.sp, s.sp));
+  const double ntm = fma(-d, s.tp, d1 * s.sp);  // shares T+ (slot B) with nsp
+  const double nsm = fma(d, s.tm, s2 * s.sm);
+  const double ntp = fma(d2, s.tm, fma(c, s.sm, -s.sm));  // shares T- (slot B) with nsm
+#endif
   s.sp = nsp;
   s.tp = ntp;
   s.sm = nsm;
@@ -705,11 +736,12 @@ static qk_status launch_sweep_ri(const SweepArgs& a, cudaStream_t st) {
   return cuda_status(cudaGetLastError(), "sweep launch");
 }
 
-// Micro-tile rows per thread: QK_SWEEP_RI=2 selects the 512-thread variant (tuning knob).
+// Micro-tile rows per thread: 2 (512 threads, 126 registers, 16 warps/SM; measured best) or
+// 4 (256 threads, 4x4 micro-tiles); QK_SWEEP_RI=4 selects the latter (tuning knob).
 static int sweep_ri() {
   static int ri = [] {
     const char* v = getenv("QK_SWEEP_RI");
-    return (v != nullptr && v[0] == '2') ? 2 : 4;
+    return (v != nullptr && v[0] == '4') ? 4 : 2;
   }();
   return ri;
 }
