@@ -42,6 +42,12 @@ struct Geo {
 };
 constexpr int kChunkElems = kChunk * kTile;            // double2 per block-chunk
 constexpr uint32_t kChunkBytes = kChunkElems * 16;     // 16 KB
+#ifndef QK_QUNROLL
+#define QK_QUNROLL 8
+#endif
+// qubits unrolled per inner iteration (tuning knob; config-4 bench with RI = 2: 1 -> 1.175,
+// 2 -> 1.212, 4 -> 1.222, 8 -> 1.233, 16 -> 1.215 G entries/s)
+constexpr int kQUnroll = QK_QUNROLL;
 constexpr int kTileTable = 512;  // per-CTA decoded tile coordinates cached in shared memory
 constexpr size_t kSmemBytes =
     size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8 + kTileTable * 8;  // ring, barriers, table
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       mbar_wait(&full[stage], uint32_t((f / kStages) & 1));
       const double2* sI = sbuf + size_t(stage) * 2 * kChunkElems;
       const double2* sJ = sI + kChunkElems;
-#pragma unroll 4
+#pragma unroll(kQUnroll)
       for (int q = 0; q < kChunk; ++q) {
         double2 vi[kRI], vj[kRJ];
 #pragma unroll
