@@ -223,8 +223,7 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2405_02630_b200 import (FeatureMapConfig, compute_cross_kernel,
-                                       compute_kernel_matrix, plan_for)
+    from paper_2405_02630_b200 import FeatureMapConfig, compute_kernel_matrices, plan_for
     from paper_2405_02630_b200 import device as qdev
     from paper_2405_02630_b200.distributed import KernelJob
 
@@ -239,7 +238,8 @@ def run_ours(args):
 
     # Instrument the sweep launches with CUDA events on the launching (current) stream.
     sweep_events = []
-    orig = {k: getattr(qdev, k) for k in ("gram", "cross", "gram_into", "cross_into")}
+    orig = {k: getattr(qdev, k) for k in ("gram", "cross", "gram_into", "cross_into",
+                                           "job_into")}
 
     def timed(fn):
         def wrap(*a, **k):
@@ -320,7 +320,8 @@ def run_ours(args):
         pass
     roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_nominal,
                 "unit": "TFLOP/s", "frac": (achieved_tf / peak_nominal) if achieved_tf else None,
-                "traffic": traffic, "kernel": "qk::sweep_kernel<2,*,0>",
+                "traffic": traffic,
+                "kernel": "qk::sweep_kernel<2,kModeJob,dense,RI=2> (Gram + cross tile list)",
                 "flops_per_entry_executed": info["flops_per_entry"],
                 "flops_per_entry_algorithmic_F": info["algorithmic_flops_per_entry"],
                 "dp_instr_per_entry": info["dp_instr_per_entry"],
@@ -347,11 +348,8 @@ def run_ours(args):
         if world == 1:
             h_K = torch.empty((N_TRAIN, N_TRAIN), dtype=torch.float64, pin_memory=True).numpy()
             h_Kx = torch.empty((N_TEST, N_TRAIN), dtype=torch.float64, pin_memory=True).numpy()
-            h2d += h_tr.nbytes  # the cross call uploads the train angles again
-
             def e2e_step():
-                compute_kernel_matrix(h_tr, cfg, out=h_K)
-                compute_cross_kernel(h_te, h_tr, cfg, out=h_Kx)
+                compute_kernel_matrices(h_tr, h_te, cfg, out_train=h_K, out_test=h_Kx)
         else:
             h_K = torch.empty((N_TRAIN, N_TRAIN), dtype=torch.float64,
                               pin_memory=True) if rank == 0 else None
@@ -380,7 +378,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(h2d * (world if world > 1 else 1)),
                "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                "ms_per_step": 1e3 * e_el / args.e2e_steps,
-               "api": "compute_kernel_matrix + compute_cross_kernel (C-ABI host pipeline)"
+               "api": "compute_kernel_matrices(train, test) (C-ABI host pipeline "
+                      "qk_kernel_matrices_host, pinned buffers)"
                if world == 1 else "KernelJob (sweeps store into rank 0 over NVLink) + pinned "
                                   "H2D/D2H"}
 

@@ -122,6 +122,14 @@ qk_status qk_cross_tiles(const qk_plan* plan, const void* d_planes_rows, int64_t
 qk_status qk_unpack_cross(const qk_plan* plan, const double* d_packed, int64_t n_rows,
                           int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                           int64_t ld, void* stream);
+/* Train Gram + test-versus-train block as ONE tile list (tiles [0, qk_gram_tile_count) are the
+ * Gram's, the rest the cross block's), one persistent launch for any sub-range — the QSVM
+ * train/test kernel pair of Algorithm 2.  Dense outputs: d_K_train is
+ * n_train x n_train (symmetrised, unit diagonal), d_K_cross is n_test x n_train. */
+int64_t qk_job_tile_count(const qk_plan* plan, int64_t n_train, int64_t n_test);
+qk_status qk_job_tiles(const qk_plan* plan, const void* d_planes_train, int64_t n_train,
+                       const void* d_planes_test, int64_t n_test, int64_t tile_begin,
+                       int64_t tile_end, double* d_K_train, double* d_K_cross, void* stream);
 /* contract_batch drop-in (engine.py:132-166): signed real amplitudes
  * <0|U(a_p)^dag U(b_q)|0> for an explicit list of index pairs d_pairs[k] = (p, q),
  * output order = input order. */
@@ -137,6 +145,11 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
                                 double* h_K);
 qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_t n_rows,
                                const double* h_cols, int64_t n_cols, double* h_K);
+/* Both of the above in one pipeline (one upload of the train angles, one sweep launch over the
+ * joint tile list, both matrices drained while it runs). */
+qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, int64_t n_train,
+                                  const double* h_test, int64_t n_test, double* h_K_train,
+                                  double* h_K_cross);
 
 /* ---- measurement helper: fp64 FMA issue-rate microbenchmark (FLOP/s) ------------- */
 qk_status qk_dfma_peak(double* out_flops_per_s, void* stream);

@@ -60,6 +60,11 @@ _SIGNATURES = {
     "qk_kernel_matrix_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp]),
     "qk_cross_kernel_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp]),
     "qk_dfma_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), _c_vp]),
+    "qk_job_tile_count": (_c_i64, [_c_vp, _c_i64, _c_i64]),
+    "qk_job_tiles": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp,
+                                    _c_vp, _c_vp]),
+    "qk_kernel_matrices_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp,
+                                               _c_vp]),
     "qk_shared_alloc": (ctypes.c_int, [_c_sz, ctypes.POINTER(_c_vp)]),
     "qk_shared_free": (ctypes.c_int, [_c_vp]),
     "qk_ipc_export": (ctypes.c_int, [_c_vp, ctypes.c_char_p]),

@@ -347,43 +347,60 @@ StreamWaitValue32Fn stream_wait_value32() {
   return fn;
 }
 
-// Launches the sweep over [0, n_tiles) on w->stream and copies row panels of d_K (row-major,
-// n_cols wide) to h_K on w->copy_stream as their super-rows complete.
-qk_status sweep_and_drain(Workspace* w, const Plan& p, int mode, const void* d_rows,
-                          int64_t n_rows, const void* d_cols, int64_t n_cols, double* d_K,
-                          double* h_K) {
-  const int64_t nbr = blocks_for(n_rows), nbc = blocks_for(n_cols);
-  const int64_t n_super = (nbr + kGroup - 1) / kGroup;
-  const int64_t n_tiles = mode == kModeGram ? nbr * (nbr + 1) / 2 : nbr * nbc;
-  const bool pinned = is_pinned(h_K);
-  const size_t row_bytes = size_t(n_cols) * sizeof(double);
-  const size_t panel_bytes = size_t(kGroup) * kTile * row_bytes;
-  if (!pinned)
-    if (qk_status s = w->ensure_stage(panel_bytes)) return s;
+// One row-major result matrix a sweep launch fills and the copy stream drains to the host.
+struct DrainTarget {
+  double* d_K;
+  double* h_K;
+  int64_t n_rows, n_cols;
+  int mode;              // kModeGram or kModeCross: how tiles map onto super-rows
+  unsigned int* d_prog;  // per-super-row finished-tile counters (set by run_and_drain)
+};
+
+// Resets the progress counters, runs `launch` (which must pass targets[k].d_prog to the
+// sweep) on w->stream, and copies each target's row panels (kGroup tile rows) to the host
+// on w->copy_stream as soon as their counters are complete — targets in order, panels in
+// row order, matching the order in which the persistent sweep finishes tiles.
+template <class Launch>
+qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targets,
+                        Launch&& launch) {
   StreamWaitValue32Fn wait = stream_wait_value32();
-  unsigned int* d_prog = nullptr;
+  int64_t n_super_total = 0;
+  bool all_pinned = true;
+  size_t panel_bytes = 0;
+  for (int k = 0; k < n_targets; ++k) {
+    n_super_total += (blocks_for(tg[k].n_rows) + kGroup - 1) / kGroup;
+    all_pinned = all_pinned && is_pinned(tg[k].h_K);
+    panel_bytes = std::max(panel_bytes, size_t(kGroup) * kTile * tg[k].n_cols * sizeof(double));
+  }
+  if (!all_pinned)
+    if (qk_status s = w->ensure_stage(panel_bytes)) return s;
   if (wait != nullptr) {
-    if (qk_status s = w->ensure(3, size_t(n_super) * sizeof(unsigned int))) return s;
-    d_prog = static_cast<unsigned int*>(w->buf[3]);
-    if (cudaError_t e = cudaMemsetAsync(d_prog, 0, size_t(n_super) * 4, w->stream))
+    if (qk_status s = w->ensure(3, size_t(n_super_total) * sizeof(unsigned int))) return s;
+    unsigned int* base = static_cast<unsigned int*>(w->buf[3]);
+    if (cudaError_t e = cudaMemsetAsync(base, 0, size_t(n_super_total) * 4, w->stream))
       return cuda_err(e, "progress reset");
+    for (int k = 0; k < n_targets; ++k) {
+      tg[k].d_prog = base;
+      base += (blocks_for(tg[k].n_rows) + kGroup - 1) / kGroup;
+    }
+  } else {
+    for (int k = 0; k < n_targets; ++k) tg[k].d_prog = nullptr;
   }
   // the copy stream may start waiting on the counters once they are reset (NOT once the
   // sweep finished: the event is recorded before the launch)
   cudaEvent_t reset;
   cudaEventCreateWithFlags(&reset, cudaEventDisableTiming);
   cudaEventRecord(reset, w->stream);
-  if (qk_status s = launch_sweep(p, mode, d_rows, n_rows, d_cols, n_cols, 0, n_tiles, d_K,
-                                 n_cols, QK_OUT_DENSE, w->stream, d_prog)) {
+  if (qk_status s = launch()) {
     cudaEventDestroy(reset);
     return s;
   }
   cudaStream_t cs = w->copy_stream;
-  if (!pinned) {  // the staging slots may still feed the H2D of the inputs
+  if (!all_pinned) {  // the staging slots may still feed the H2D of the inputs
     for (int k = 0; k < 2; ++k)
       if (w->stage_ev[k]) cudaStreamWaitEvent(cs, w->stage_ev[k], 0);
   }
-  if (d_prog != nullptr) {
+  if (wait != nullptr) {
     cudaStreamWaitEvent(cs, reset, 0);
   } else {
     cudaEvent_t fin;  // no stream memory ops: drain after the sweep
@@ -393,48 +410,61 @@ qk_status sweep_and_drain(Workspace* w, const Plan& p, int mode, const void* d_r
     cudaEventDestroy(fin);
   }
   cudaStreamQuery(w->stream);  // flush the launch to the device before host-blocking work
-  cudaError_t e = cudaSuccess;
-  auto rows_of = [&](int64_t sr, int64_t& i0, int64_t& i1) {
+  // flat list of panels (target, super-row)
+  std::vector<std::pair<int, int64_t>> panels;
+  for (int k = 0; k < n_targets; ++k)
+    for (int64_t sr = 0; sr < (blocks_for(tg[k].n_rows) + kGroup - 1) / kGroup; ++sr)
+      panels.emplace_back(k, sr);
+  const uint32_t unit = p.layers >= 3 ? 16u : 1u;  // L >= 3 counts 16 sub-tiles per tile
+  auto rows_of = [&](int k, int64_t sr, int64_t& i0, int64_t& i1) {
     i0 = sr * kGroup * kTile;
-    i1 = std::min<int64_t>((sr + 1) * kGroup * kTile, n_rows);
+    i1 = std::min<int64_t>((sr + 1) * kGroup * kTile, tg[k].n_rows);
   };
-  auto enqueue = [&](int64_t sr, void* dst) -> cudaError_t {
-    if (d_prog != nullptr) {
+  auto enqueue = [&](size_t idx, void* dst) -> cudaError_t {
+    const int k = panels[idx].first;
+    const int64_t sr = panels[idx].second;
+    const DrainTarget& t = tg[k];
+    if (t.d_prog != nullptr) {
+      const int64_t nbr = blocks_for(t.n_rows), nbc = blocks_for(t.n_cols);
       const int64_t r0 = sr * kGroup, r1 = std::min<int64_t>(r0 + kGroup, nbr);
-      const uint32_t unit = p.layers >= 3 ? 16u : 1u;  // L >= 3 counts 16 sub-tiles per tile
-      const uint32_t expect = unit * uint32_t(mode == kModeGram
-                                                  ? upper_row_offset(r1, nbr) -
-                                                        upper_row_offset(r0, nbr)
-                                                  : (r1 - r0) * nbc);
-      if (wait(cs, reinterpret_cast<uintptr_t>(d_prog + sr), expect, 0x0) != 0)
+      const uint32_t expect =
+          unit * uint32_t(t.mode == kModeGram
+                              ? upper_row_offset(r1, nbr) - upper_row_offset(r0, nbr)
+                              : (r1 - r0) * nbc);
+      if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + sr), expect, 0x0) != 0)
         return cudaErrorNotSupported;
     }
     int64_t i0, i1;
-    rows_of(sr, i0, i1);
-    return cudaMemcpyAsync(dst, d_K + i0 * n_cols, size_t(i1 - i0) * row_bytes,
-                           cudaMemcpyDeviceToHost, cs);
+    rows_of(k, sr, i0, i1);
+    return cudaMemcpyAsync(dst, t.d_K + i0 * t.n_cols,
+                           size_t(i1 - i0) * t.n_cols * sizeof(double), cudaMemcpyDeviceToHost,
+                           cs);
   };
-  if (pinned) {
-    for (int64_t sr = 0; sr < n_super && e == cudaSuccess; ++sr) {
+  cudaError_t e = cudaSuccess;
+  const size_t np = panels.size();
+  if (all_pinned) {
+    for (size_t idx = 0; idx < np && e == cudaSuccess; ++idx) {
       int64_t i0, i1;
-      rows_of(sr, i0, i1);
-      e = enqueue(sr, h_K + i0 * n_cols);
+      rows_of(panels[idx].first, panels[idx].second, i0, i1);
+      e = enqueue(idx, tg[panels[idx].first].h_K + i0 * tg[panels[idx].first].n_cols);
     }
   } else {
-    // two pinned slots: DMA panel sr+2 while the pool copies panel sr into the user buffer
-    for (int64_t sr = 0; sr < std::min<int64_t>(2, n_super) && e == cudaSuccess; ++sr) {
-      e = enqueue(sr, w->stage[sr & 1]);
-      if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[sr & 1], cs);
+    // two pinned slots: DMA panel idx+2 while the pool copies panel idx into the user buffer
+    for (size_t idx = 0; idx < std::min<size_t>(2, np) && e == cudaSuccess; ++idx) {
+      e = enqueue(idx, w->stage[idx & 1]);
+      if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[idx & 1], cs);
     }
-    for (int64_t sr = 0; sr < n_super && e == cudaSuccess; ++sr) {
-      const int slot = int(sr & 1);
+    for (size_t idx = 0; idx < np && e == cudaSuccess; ++idx) {
+      const int slot = int(idx & 1);
       e = cudaEventSynchronize(w->stage_ev[slot]);
       if (e != cudaSuccess) break;
+      const DrainTarget& t = tg[panels[idx].first];
       int64_t i0, i1;
-      rows_of(sr, i0, i1);
-      copy_pool().copy(h_K + i0 * n_cols, w->stage[slot], size_t(i1 - i0) * row_bytes);
-      if (sr + 2 < n_super) {
-        e = enqueue(sr + 2, w->stage[slot]);
+      rows_of(panels[idx].first, panels[idx].second, i0, i1);
+      copy_pool().copy(t.h_K + i0 * t.n_cols, w->stage[slot],
+                       size_t(i1 - i0) * t.n_cols * sizeof(double));
+      if (idx + 2 < np) {
+        e = enqueue(idx + 2, w->stage[slot]);
         if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[slot], cs);
       }
     }
@@ -472,8 +502,13 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
-  if (qk_status s = sweep_and_drain(w, *p, kModeGram, w->buf[1], N, w->buf[1], N,
-                                    static_cast<double*>(w->buf[2]), h_K))
+  DrainTarget tg[1] = {{static_cast<double*>(w->buf[2]), h_K, N, N, kModeGram, nullptr}};
+  void* planes = w->buf[1];
+  if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
+        return launch_sweep(*p, kModeGram, planes, N, planes, N, 0,
+                            qk_gram_tile_count(plan, N), tg[0].d_K, N, QK_OUT_DENSE, w->stream,
+                            tg[0].d_prog);
+      }))
     return s;
   static const char* const names[1] = {"train"};
   return check_bad(w->bad, 1, names);
@@ -507,11 +542,84 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
   if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st)) return s;
-  if (qk_status s = sweep_and_drain(w, *p, kModeCross, dPr, n_rows, dPc, n_cols,
-                                    static_cast<double*>(w->buf[2]), h_K))
+  DrainTarget tg[1] = {
+      {static_cast<double*>(w->buf[2]), h_K, n_rows, n_cols, kModeCross, nullptr}};
+  if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
+        return launch_sweep(*p, kModeCross, dPr, n_rows, dPc, n_cols, 0,
+                            qk_cross_tile_count(plan, n_rows, n_cols), tg[0].d_K, n_cols,
+                            QK_OUT_DENSE, w->stream, tg[0].d_prog);
+      }))
     return s;
   static const char* const names[2] = {"test", "train"};
   return check_bad(w->bad, 2, names);
+}
+
+qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, int64_t n_train,
+                                  const double* h_test, int64_t n_test, double* h_K_train,
+                                  double* h_K_cross) {
+  const Plan* p;
+  if (qk_status s = check_plan(plan, &p)) return s;
+  if (n_train < 0 || n_test < 0) return set_error(QK_ERR_VALUE, "negative size");
+  if (n_train == 0) return QK_OK;
+  if (!h_train || !h_K_train || (n_test > 0 && (!h_test || !h_K_cross)))
+    return set_error(QK_ERR_VALUE, "NULL host buffer");
+  Workspace* w;
+  std::unique_lock<std::mutex> lock;
+  if (qk_status s = workspace_for_current(&w, lock)) return s;
+  const size_t xtb = size_t(n_train) * p->width * sizeof(double);
+  const size_t xsb = size_t(n_test) * p->width * sizeof(double);
+  const size_t ptb = qk_planes_bytes(plan, n_train);
+  const size_t psb = qk_planes_bytes(plan, n_test);
+  const size_t ktb = size_t(n_train) * size_t(n_train) * sizeof(double);
+  const size_t ksb = size_t(n_test) * size_t(n_train) * sizeof(double);
+  if (qk_status s = w->ensure(0, xtb + xsb)) return s;
+  if (qk_status s = w->ensure(1, ptb + psb)) return s;
+  if (qk_status s = w->ensure(2, ktb + ksb)) return s;
+  double* dXt = static_cast<double*>(w->buf[0]);
+  double* dXs = dXt + size_t(n_train) * p->width;
+  char* dPt = static_cast<char*>(w->buf[1]);
+  char* dPs = dPt + ptb;
+  double* dKt = static_cast<double*>(w->buf[2]);
+  double* dKs = dKt + size_t(n_train) * size_t(n_train);
+  cudaStream_t st = w->stream;
+  if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
+  if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
+  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+    return cuda_err(e, "sentinel reset");
+  if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
+  if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st)) return s;
+  DrainTarget tg[2] = {{dKt, h_K_train, n_train, n_train, kModeGram, nullptr},
+                       {dKs, h_K_cross, n_test, n_train, kModeCross, nullptr}};
+  const int64_t nt = qk_job_tile_count(plan, n_train, n_test);
+  if (qk_status s = run_and_drain(w, *p, tg, n_test > 0 ? 2 : 1, [&] {
+        return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
+                          tg[1].d_prog);
+      }))
+    return s;
+  static const char* const names[2] = {"train", "test"};
+  return check_bad(w->bad, 2, names);
+}
+
+int64_t qk_job_tile_count(const qk_plan* plan, int64_t n_train, int64_t n_test) {
+  if (plan == nullptr || n_train < 0 || n_test < 0) return 0;
+  return qk_gram_tile_count(plan, n_train) + qk_cross_tile_count(plan, n_test, n_train);
+}
+
+qk_status qk_job_tiles(const qk_plan* plan, const void* d_planes_train, int64_t n_train,
+                       const void* d_planes_test, int64_t n_test, int64_t tile_begin,
+                       int64_t tile_end, double* d_K_train, double* d_K_cross, void* stream) {
+  const Plan* p;
+  if (qk_status s = check_plan(plan, &p)) return s;
+  const int64_t nt = qk_job_tile_count(plan, n_train, n_test);
+  if (n_train < 0 || n_test < 0 || tile_begin < 0 || tile_end < tile_begin || tile_end > nt)
+    return set_error(QK_ERR_VALUE, "tile range outside the job tile list");
+  if (tile_end == tile_begin) return QK_OK;
+  if (!d_planes_train || !d_K_train || (n_test > 0 && (!d_planes_test || !d_K_cross)))
+    return set_error(QK_ERR_VALUE, "NULL buffer");
+  if (!aligned16(d_planes_train) || (n_test > 0 && !aligned16(d_planes_test)))
+    return set_error(QK_ERR_VALUE, "planes must be 16-byte aligned");
+  return launch_job(*p, d_planes_train, n_train, d_planes_test, n_test, tile_begin, tile_end,
+                    d_K_train, d_K_cross, stream);
 }
 
 }  // extern "C"

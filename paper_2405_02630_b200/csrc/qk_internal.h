@@ -53,7 +53,14 @@ qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* 
                        const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream);
 qk_status launch_dfma_peak(double* out, void* stream);
 
-enum SweepMode { kModeGram = 0, kModeCross = 1 };
+enum SweepMode { kModeGram = 0, kModeCross = 1, kModeJob = 2 };
+
+// Train Gram + test-versus-train cross block as ONE tile list: tiles [0, gram_tiles) are the
+// Gram's, the rest the cross block's (dense outputs; optional per-super-row progress).
+qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
+                     int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
+                     double* d_K_cross, void* stream, unsigned int* d_prog_train = nullptr,
+                     unsigned int* d_prog_cross = nullptr);
 
 }  // namespace qk
 

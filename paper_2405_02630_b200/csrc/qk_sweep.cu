@@ -404,6 +404,18 @@ struct SweepArgs {
   double final_scale;
   int n_pad, nchunks, convention;
   unsigned int* progress;  // optional: per-super-row count of finished tiles (host pipelines)
+  // kModeJob: tiles [0, n_first) are the Gram of (rows = cols); the rest the cross block
+  // rows2 x cols (rows2 = test planes) stored to out2 (ld = n_cols), counted in progress2.
+  const double2* rows2;
+  int64_t n_rows2, nb_rows2, n_first;
+  double* out2;
+  unsigned int* progress2;
+};
+
+// Per-tile coordinates: tile rows/cols in plane blocks and which problem of a kModeJob launch.
+struct TileXY {
+  int64_t bi, bj;
+  int prob;
 };
 
 template <int LAYERS, int MODE, int OUT, int RI>
@@ -423,38 +435,41 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   const int64_t F = my_tiles * nchunks;
 
   int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
-  auto decode = [&](int64_t k, int64_t& bi, int64_t& bj) {
+  auto decode = [&](int64_t k) -> TileXY {
     const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
-    if (MODE == kModeGram) {
-      decode_upper(g, a.nb_rows, bi, bj);
+    TileXY t;
+    t.prob = 0;
+    if (MODE == kModeGram || (MODE == kModeJob && g < a.n_first)) {
+      decode_upper(g, a.nb_rows, t.bi, t.bj);
+    } else if (MODE == kModeCross) {
+      decode_rect(g, a.nb_rows, a.nb_cols, t.bi, t.bj);
     } else {
-      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+      decode_rect(g - a.n_first, a.nb_rows2, a.nb_cols, t.bi, t.bj);
+      t.prob = 1;
     }
+    return t;
   };
-  auto tile_of = [&](int64_t k, int64_t& bi, int64_t& bj) {
+  auto tile_of = [&](int64_t k) -> TileXY {
     if (k < kTileTable) {
-      const int2 t = table[k];
-      bi = t.x;
-      bj = t.y;
-    } else {
-      decode(k, bi, bj);
+      const int2 e = table[k];
+      return TileXY{e.x & 0x3fffffff, e.y, e.x >> 30};
     }
+    return decode(k);
   };
   for (int64_t k = tid; k < my_tiles && k < kTileTable; k += blockDim.x) {
-    int64_t bi, bj;
-    decode(k, bi, bj);
-    table[k] = make_int2(int(bi), int(bj));
+    const TileXY t = decode(k);
+    table[k] = make_int2(int(t.bi) | (t.prob << 30), int(t.bj));
   }
   __syncthreads();
   auto issue = [&](int64_t f) {  // fill stage f % kStages with item f
     const int64_t k = f / nchunks;
     const int c = int(f - k * nchunks);
-    int64_t bi, bj;
-    tile_of(k, bi, bj);
+    const TileXY t = tile_of(k);
     const int stage = int(f % kStages);
     double2* dst = sbuf + size_t(stage) * 2 * kChunkElems;
-    const double2* si = a.rows + (bi * a.n_pad + int64_t(c) * kChunk) * kTile;
-    const double2* sj = a.cols + (bj * a.n_pad + int64_t(c) * kChunk) * kTile;
+    const double2* si =
+        (t.prob ? a.rows2 : a.rows) + (t.bi * a.n_pad + int64_t(c) * kChunk) * kTile;
+    const double2* sj = a.cols + (t.bj * a.n_pad + int64_t(c) * kChunk) * kTile;
     mbar_arrive_expect_tx(&full[stage], 2 * kChunkBytes);
     bulk_g2s(dst, si, kChunkBytes, &full[stage]);
     bulk_g2s(dst + kChunkElems, sj, kChunkBytes, &full[stage]);
@@ -514,8 +529,9 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     }
 
     // ---- epilogue ----
-    int64_t bi, bj;
-    tile_of(k, bi, bj);
+    const TileXY t = tile_of(k);
+    const int64_t bi = t.bi, bj = t.bj;
+    const bool gram = MODE == kModeGram || (MODE == kModeJob && t.prob == 0);
     if (OUT == QK_OUT_PACKED) {
       const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
       double* o = a.out + (g - a.tile_begin) * int64_t(kTile * kTile);
@@ -526,6 +542,9 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
           o[(ty + kTY * r) * kTile + tx + kTX * c] =
               kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
     } else {
+      double* out = t.prob ? a.out2 : a.out;
+      const int64_t ld = t.prob ? a.n_cols : a.ld_out;
+      const int64_t n_rows = t.prob ? a.n_rows2 : a.n_rows;
 #pragma unroll
       for (int r = 0; r < kRI; ++r) {
         const int64_t i = bi * kTile + ty + kTY * r;
@@ -533,26 +552,27 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         for (int c = 0; c < kRJ; ++c) {
           const int64_t j = bj * kTile + tx + kTX * c;
           const double v = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
-          if (MODE == kModeGram) {
-            if (i < a.n_rows && j < a.n_rows) {
+          if (gram) {
+            if (i < n_rows && j < n_rows) {
               if (i < j) {
-                a.out[i * a.ld_out + j] = v;
-                a.out[j * a.ld_out + i] = v;
+                out[i * ld + j] = v;
+                out[j * ld + i] = v;
               } else if (i == j) {
-                a.out[i * a.ld_out + i] = 1.0;
+                out[i * ld + i] = 1.0;
               }
             }
           } else {
-            if (i < a.n_rows && j < a.n_cols) a.out[i * a.ld_out + j] = v;
+            if (i < n_rows && j < a.n_cols) out[i * ld + j] = v;
           }
         }
       }
     }
-    if (a.progress != nullptr) {
+    unsigned int* prog = t.prob ? a.progress2 : a.progress;
+    if (prog != nullptr) {
       // publish the finished tile to a copy stream waiting on its super-row counter
       __threadfence_system();
       __syncthreads();
-      if (tid == 0) atomicAdd(a.progress + bi / kGroup, 1u);
+      if (tid == 0) atomicAdd(prog + bi / kGroup, 1u);
     }
   }
 }
@@ -777,7 +797,7 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
                        unsigned int* d_progress) {
   if (tile_end <= tile_begin) return QK_OK;
-  SweepArgs a;
+  SweepArgs a{};
   a.progress = d_progress;
   a.rows = static_cast<const double2*>(d_rows);
   a.cols = static_cast<const double2*>(d_cols);
@@ -814,6 +834,51 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
                   : launch_general<3, kModeGram, QK_OUT_DENSE>(a, st);
   return packed ? launch_general<3, kModeCross, QK_OUT_PACKED>(a, st)
                 : launch_general<3, kModeCross, QK_OUT_DENSE>(a, st);
+}
+
+qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
+                     int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
+                     double* d_K_cross, void* stream, unsigned int* d_prog_train,
+                     unsigned int* d_prog_cross) {
+  if (tile_end <= tile_begin) return QK_OK;
+  const int64_t nbt = blocks_for(n_train);
+  const int64_t n_gram = nbt * (nbt + 1) / 2;
+  if (p.layers == 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
+    // one problem only (or the one-pair-per-thread L = 3 kernel): plain launches
+    if (qk_status s = launch_sweep(p, kModeGram, d_train, n_train, d_train, n_train, tile_begin,
+                                   std::min(tile_end, n_gram), d_K_train, n_train,
+                                   QK_OUT_DENSE, stream, d_prog_train))
+      return s;
+    if (n_test == 0 || tile_end <= n_gram) return QK_OK;
+    return launch_sweep(p, kModeCross, d_test, n_test, d_train, n_train,
+                        std::max(tile_begin, n_gram) - n_gram, tile_end - n_gram, d_K_cross,
+                        n_train, QK_OUT_DENSE, stream, d_prog_cross);
+  }
+  SweepArgs a{};
+  a.rows = static_cast<const double2*>(d_train);
+  a.cols = static_cast<const double2*>(d_train);
+  a.n_rows = n_train;
+  a.n_cols = n_train;
+  a.nb_rows = nbt;
+  a.nb_cols = nbt;
+  a.tile_begin = tile_begin;
+  a.n_tiles = tile_end - tile_begin;
+  a.out = d_K_train;
+  a.ld_out = n_train;
+  a.final_scale = p.final_scale;
+  a.n_pad = p.width_padded;
+  a.nchunks = p.width_padded / kChunk;
+  a.convention = p.convention;
+  a.progress = d_prog_train;
+  a.rows2 = static_cast<const double2*>(d_test);
+  a.n_rows2 = n_test;
+  a.nb_rows2 = blocks_for(n_test);
+  a.n_first = n_gram;
+  a.out2 = d_K_cross;
+  a.progress2 = d_prog_cross;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p.layers == 2) return launch_sweep_t<2, kModeJob, QK_OUT_DENSE>(a, st);
+  return launch_sweep_t<1, kModeJob, QK_OUT_DENSE>(a, st);
 }
 
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,

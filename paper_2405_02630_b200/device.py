@@ -122,6 +122,20 @@ def cross_into(rows: Planes, cols: Planes, out_ptr: int, tile_begin: int, tile_e
                                                _native.QK_OUT_DENSE, _stream()))
 
 
+def job_into(train: Planes, test: Planes | None, K_train_ptr: int, K_cross_ptr: int,
+             tile_begin: int = 0, tile_end: int | None = None) -> None:
+    """Train Gram + test x train block as one tile list, one persistent launch, dense outputs
+    at raw device addresses (row-major N_train x N_train and N_test x N_train)."""
+    plan = train.plan
+    n_test = test.n if test is not None else 0
+    nt = int(_native.lib().qk_job_tile_count(plan.handle, train.n, n_test))
+    tile_end = nt if tile_end is None else tile_end
+    _native.check(_native.lib().qk_job_tiles(plan.handle, train.ptr(), train.n,
+                                             test.ptr() if test is not None else None, n_test,
+                                             tile_begin, tile_end, K_train_ptr,
+                                             K_cross_ptr if n_test else None, _stream()))
+
+
 def unpack_gram(plan: SweepPlan, packed: torch.Tensor, n: int, tile_begin: int, tile_end: int,
                 K: torch.Tensor) -> torch.Tensor:
     _require(packed, "packed", torch.float64)

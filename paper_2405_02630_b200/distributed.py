@@ -178,9 +178,8 @@ class KernelJob:
             if lay.n_test:
                 self.K_cross = torch.empty((lay.n_test, lay.n_train), dtype=torch.float64,
                                            device=devc)
-        dev.gram(p_train, out=self.K_train)
-        if lay.n_test:
-            dev.cross(p_test, p_train, out=self.K_cross)
+        dev.job_into(p_train, p_test, self.K_train.data_ptr(),
+                     self.K_cross.data_ptr() if lay.n_test else 0)
         return self.K_train, self.K_cross
 
     # ---- p2p placement: sweeps store into rank 0's matrices ----------------------------
@@ -209,12 +208,9 @@ class KernelJob:
         if self._shared is None:
             self._setup_shared()
         lay = self.layout
-        for seg in lay.segments(self.rank):
-            if seg.kind == "gram":
-                dev.gram_into(p_train, self._shared[0].ptr, seg.tile_begin, seg.tile_end)
-            else:
-                dev.cross_into(p_test, p_train, self._shared[1].ptr, seg.tile_begin,
-                               seg.tile_end)
+        lo, hi = lay.union_range(self.rank)  # one launch over this rank's joint tile range
+        dev.job_into(p_train, p_test, self._shared[0].ptr,
+                     self._shared[1].ptr if lay.n_test else 0, lo, hi)
         torch.cuda.current_stream().synchronize()  # this rank's stores have landed
         dist.barrier(group=self.group)
         if self.rank != 0:

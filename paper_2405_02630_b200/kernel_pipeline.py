@@ -277,6 +277,50 @@ def compute_cross_kernel(test, train, cfg, plan=None, workers: int = 1, *,
     return KernelMatrix(Nt, Nr, out, convention, _metadata(cfg, sp, dataset_id, "cross"))
 
 
+def compute_kernel_matrices(train, test, cfg, plan=None, workers: int = 1, *,
+                            convention: str = "probability", dataset_id: str | None = None,
+                            out_train: np.ndarray | None = None,
+                            out_test: np.ndarray | None = None):
+    """The QSVM train/test kernel pair of Algorithm 2 in one call:
+    ``(compute_kernel_matrix(train), compute_cross_kernel(test, train))`` with identical
+    results, computed as ONE sweep over the joint tile list (one upload of the train angles,
+    both matrices drained to the host while the sweep runs)."""
+    cfg = as_config(cfg)
+    convention = check_convention(convention)
+    _check_workers(workers)
+    sp = _resolve_plan(cfg, plan, convention)
+    if _is_cuda_tensor(train) or _is_cuda_tensor(test):
+        return (_compute_kernel_matrix_device(train, cfg, sp, convention, dataset_id),
+                _compute_cross_kernel_device(test, train, cfg, sp, convention, dataset_id))
+    R = _host_angles(train, cfg.width)
+    T = _host_angles(test, cfg.width)
+    Nr, Nt = R.shape[0], T.shape[0]
+    if Nr and (R.shape[1] != cfg.width or (Nt and T.shape[1] != cfg.width)):
+        raise _width_error(R.shape[1], T.shape[1] if Nt else R.shape[1], cfg.width)
+    K = host_empty((Nr, Nr)) if out_train is None else out_train
+    Kx = host_empty((Nt, Nr)) if out_test is None else out_test
+    for arr, shape in ((K, (Nr, Nr)), (Kx, (Nt, Nr))):
+        if arr.shape != shape or arr.dtype != np.float64 or not arr.flags.c_contiguous:
+            raise ValueError(f"outputs must be C-contiguous float64 arrays of shape {shape}")
+    if Nr == 1:
+        K[0, 0] = 1.0
+    if Nr >= 2 or (Nr and Nt):
+        status = _native.lib().qk_kernel_matrices_host(sp.handle, R.ctypes.data, Nr,
+                                                       T.ctypes.data, Nt, K.ctypes.data,
+                                                       Kx.ctypes.data)
+        if status == _native.QK_ERR_REBIND:
+            if not np.isfinite(R).all() and Nr >= 2:
+                raise RebindError(f"operand set {_first_bad_gram_pair(R)}: feature angles "
+                                  "must be finite")
+            raise RebindError(f"operand set {_first_bad_cross_pair(T, R)}: feature angles "
+                              "must be finite")
+        _native.check(status)
+        if Nr == 1:
+            K[0, 0] = 1.0
+    return (KernelMatrix(Nr, Nr, K, convention, _metadata(cfg, sp, dataset_id, "gram")),
+            KernelMatrix(Nt, Nr, Kx, convention, _metadata(cfg, sp, dataset_id, "cross")))
+
+
 # ---------------------------------------------------------------------------------------
 # device-resident variants (CUDA torch tensors in -> CUDA torch tensor entries)
 # ---------------------------------------------------------------------------------------

@@ -236,3 +236,26 @@ def test_shard_run_then_merge_equals_full_matrix(tmp_path, rng):
             save_partial(p, vals, rng_k, rows, N, test is None)
             paths.append(p)
         assert np.array_equal(merge_partials(paths).entries, full)
+
+
+@pytest.mark.parametrize("layers", [1, 2, 3])
+def test_joint_train_test_pass_equals_separate_calls(layers, rng):
+    """compute_kernel_matrices (one sweep over the joint tile list, host pipeline) and the
+    device job path == compute_kernel_matrix + compute_cross_kernel, bit for bit."""
+    from paper_2405_02630_b200 import compute_kernel_matrices
+
+    n = 40 if layers < 3 else 12
+    Xtr = rng.uniform(0, 0.3, (600, n))
+    Xte = rng.uniform(0, 0.3, (150, n))
+    cfg = FeatureMapConfig(n, layers=layers)
+    K, Kx = compute_kernel_matrices(Xtr, Xte, cfg)
+    assert np.array_equal(K.entries, compute_kernel_matrix(Xtr, cfg).entries)
+    assert np.array_equal(Kx.entries, compute_cross_kernel(Xte, Xtr, cfg).entries)
+    pinned_k = torch.empty((600, 600), dtype=torch.float64, pin_memory=True).numpy()
+    pinned_x = torch.empty((150, 600), dtype=torch.float64, pin_memory=True).numpy()
+    K2, Kx2 = compute_kernel_matrices(Xtr, Xte, cfg, out_train=pinned_k, out_test=pinned_x)
+    assert np.array_equal(K2.entries, K.entries) and np.array_equal(Kx2.entries, Kx.entries)
+    job = KernelJob(SweepPlan(n, layers), 600, 150)
+    Kd, Kxd = job.run(torch.as_tensor(Xtr, device="cuda"), torch.as_tensor(Xte, device="cuda"))
+    assert np.array_equal(Kd.cpu().numpy(), K.entries)
+    assert np.array_equal(Kxd.cpu().numpy(), Kx.entries)
