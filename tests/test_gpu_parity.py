@@ -259,3 +259,52 @@ def test_joint_train_test_pass_equals_separate_calls(layers, rng):
     Kd, Kxd = job.run(torch.as_tensor(Xtr, device="cuda"), torch.as_tensor(Xte, device="cuda"))
     assert np.array_equal(Kd.cpu().numpy(), K.entries)
     assert np.array_equal(Kxd.cpu().numpy(), Kx.entries)
+
+
+def test_config2_full_matrices_vs_oracle():
+    """BASELINE configs[1]: 50 qubits (PCA), 1000 train x 500 test — EVERY entry of both
+    matrices against the oracle (1e-12), and identical SVC predictions."""
+    from sklearn.svm import SVC
+
+    from paper_2405_02630_b200 import compute_kernel_matrices
+    from paper_2405_02630_b200.data import config_data
+
+    Atr, ytr, Ate, yte = config_data(2, 1000, 500, "mnist", features=50, binary=(2, 6))
+    cfg = FeatureMapConfig(50)
+    K, Kx = compute_kernel_matrices(Atr, Ate, cfg)
+    Kr, Kxr = oracle.kernel_matrix(Atr, 2), oracle.cross_kernel(Ate, Atr, 2)
+    assert np.abs(K.entries - Kr).max() <= K_ABS and np.abs(Kx.entries - Kxr).max() <= K_ABS
+    # min-max angles over [0, pi] concentrate this kernel (median K ~ 1e-10), so the
+    # absolute gate alone is weak: K = amp^2 must also agree to ~2x the amplitude gate
+    for got, ref in ((K.entries, Kr), (Kx.entries, Kxr)):
+        assert np.all(np.abs(got - ref) <= 2 * AMP_REL * ref + 1e-300)
+    p = SVC(kernel="precomputed", C=1.0).fit(K.entries, ytr).predict(Kx.entries)
+    pr = SVC(kernel="precomputed", C=1.0).fit(Kr, ytr).predict(Kxr)
+    assert np.array_equal(p, pr)
+
+
+def test_config3_fashion_784_sampled_and_ovr_accuracy():
+    """BASELINE configs[2]: Fashion-shaped, 10-class one-vs-rest, 784 qubits, 2000 x 1000 —
+    256 sampled entries of each matrix vs the oracle; identical OvR predictions from the
+    engine's K and from K with the sampled entries replaced by the oracle's values."""
+    from sklearn.multiclass import OneVsRestClassifier
+    from sklearn.svm import SVC
+
+    from paper_2405_02630_b200 import compute_kernel_matrices
+    from paper_2405_02630_b200.data import config_data
+
+    Atr, ytr, Ate, yte = config_data(3, 2000, 1000, "fashion", bw=0.02)
+    cfg = FeatureMapConfig(784)
+    K, Kx = compute_kernel_matrices(Atr, Ate, cfg)
+    rng = np.random.default_rng(11)
+    i, j = rng.integers(0, 2000, 256), rng.integers(0, 2000, 256)
+    keep = i != j
+    ref = np.abs(oracle.amplitudes(Atr, Atr, np.stack([i[keep], j[keep]], 1), 2)) ** 2
+    assert np.abs(K.entries[i[keep], j[keep]] - ref).max() <= K_ABS
+    r, c = rng.integers(0, 1000, 256), rng.integers(0, 2000, 256)
+    refx = np.abs(oracle.amplitudes(Ate, Atr, np.stack([r, c], 1), 2)) ** 2
+    assert np.abs(Kx.entries[r, c] - refx).max() <= K_ABS
+    assert 1e-3 <= np.median(ref) <= 0.9
+    clf = OneVsRestClassifier(SVC(kernel="precomputed", C=1.0)).fit(K.entries, ytr)
+    acc = float((clf.predict(Kx.entries) == yte).mean())
+    assert acc > 0.5  # 10-class synthetic Fashion: far above the 0.1 chance level
