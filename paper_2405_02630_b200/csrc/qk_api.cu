@@ -417,8 +417,10 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
       panels.emplace_back(k, sr);
   const uint32_t unit = p.layers >= 3 ? 16u : 1u;  // L >= 3 counts 16 sub-tiles per tile
   auto rows_of = [&](int k, int64_t sr, int64_t& i0, int64_t& i1) {
-    i0 = sr * kGroup * kTile;
-    i1 = std::min<int64_t>((sr + 1) * kGroup * kTile, tg[k].n_rows);
+    // sample rows of super-row sr (the front padding of block 0 is not a sample)
+    const int64_t pad = sample_pad(tg[k].n_rows);
+    i0 = std::max<int64_t>(0, sr * kGroup * kTile - pad);
+    i1 = std::min<int64_t>((sr + 1) * kGroup * kTile - pad, tg[k].n_rows);
   };
   auto enqueue = [&](size_t idx, void* dst) -> cudaError_t {
     const int k = panels[idx].first;

@@ -36,6 +36,11 @@ int64_t blocks_for(int64_t n_samples);
 #define QK_HD
 #endif
 
+// Sample padding of a plane set: the ragged remainder sits at the FRONT of block 0 (slot
+// t of block b holds sample 64 b + t - pad), so it is a tile ROW of every Gram tile that
+// touches it and whole warps of those tiles can skip it.
+QK_HD inline int sample_pad(int64_t n) { return int((kTile - n % kTile) % kTile); }
+
 // First linear index of tile row r in the upper-triangle tile list over nb blocks.
 QK_HD inline int64_t upper_row_offset(int64_t r, int64_t nb) { return r * nb - r * (r - 1) / 2; }
 

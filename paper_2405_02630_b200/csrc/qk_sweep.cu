@@ -359,12 +359,13 @@ __global__ void __launch_bounds__(256) gate_build_kernel(const double* __restric
   __shared__ double tile[kTile][33];
   const int64_t blk = blockIdx.x;
   const int q0 = blockIdx.y * 32;
+  const int spad = sample_pad(n_samples);
   for (int idx = threadIdx.x; idx < kTile * 32; idx += blockDim.x) {
     const int t = idx >> 5, qq = idx & 31;
-    const int64_t s = blk * kTile + t;
+    const int64_t s = blk * kTile + t - spad;  // padding slots (s < 0) get angle 0
     const int q = q0 + qq - front;
     double x = 0.0;
-    if (s < n_samples && q >= 0 && q < width) {
+    if (s >= 0 && s < n_samples && q >= 0 && q < width) {
       x = __ldg(X + s * ld + q);
       if (bad != nullptr && !isfinite(x)) atomicMin(bad, (unsigned long long)s);
     }
@@ -410,6 +411,7 @@ struct SweepArgs {
   int64_t n_rows2, nb_rows2, n_first;
   double* out2;
   unsigned int* progress2;
+  int pad_rows, pad_cols, pad_rows2;  // sample_pad() of each plane set (front of block 0)
 };
 
 // Per-tile coordinates: tile rows/cols in plane blocks and which problem of a kModeJob launch.
@@ -486,10 +488,18 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   __syncthreads();
 
   // ---------------- compute warps ----------------
+  // Thread (ty, tx) owns tile rows ty*kRI .. ty*kRI+kRI-1 (consecutive, so a warp covers
+  // 2*kRI whole rows) and columns tx + kTX*c.
   const int tx = tid % kTX, ty = tid / kTX;
+  const int warp_row_end = (tid / 32 + 1) * (32 / kTX) * kRI;  // rows [.., end) of this warp
   St st[kRI][kRJ];
   int64_t f = 0;
   for (int64_t k = 0; k < my_tiles; ++k) {
+    const TileXY tk = tile_of(k);
+    // padding rows of this tile (front of plane block 0): warps made only of them skip the
+    // sweep (they still release every stage) — the ragged sample block costs ~1/4 of a tile
+    const int pad_r = tk.bi == 0 ? (tk.prob ? a.pad_rows2 : a.pad_rows) : 0;
+    const bool idle = warp_row_end <= pad_r;
 #pragma unroll
     for (int r = 0; r < kRI; ++r)
 #pragma unroll
@@ -500,17 +510,19 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       mbar_wait(&full[stage], uint32_t((f / kStages) & 1));
       const double2* sI = sbuf + size_t(stage) * 2 * kChunkElems;
       const double2* sJ = sI + kChunkElems;
+      if (!idle) {
 #pragma unroll(kQUnroll)
-      for (int q = 0; q < kChunk; ++q) {
-        double2 vi[kRI], vj[kRJ];
+        for (int q = 0; q < kChunk; ++q) {
+          double2 vi[kRI], vj[kRJ];
 #pragma unroll
-        for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty + kTY * r];
+          for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty * kRI + r];
 #pragma unroll
-        for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
+          for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
 #pragma unroll
-        for (int r = 0; r < kRI; ++r)
+          for (int r = 0; r < kRI; ++r)
 #pragma unroll
-          for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+            for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+        }
       }
       __syncwarp();  // every lane's reads of this stage have completed
       if (lane == 0) {
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     }
 
     // ---- epilogue ----
-    const TileXY t = tile_of(k);
+    const TileXY t = tk;
     const int64_t bi = t.bi, bj = t.bj;
     const bool gram = MODE == kModeGram || (MODE == kModeJob && t.prob == 0);
     if (OUT == QK_OUT_PACKED) {
@@ -539,21 +551,23 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       for (int r = 0; r < kRI; ++r)
 #pragma unroll
         for (int c = 0; c < kRJ; ++c)
-          o[(ty + kTY * r) * kTile + tx + kTX * c] =
+          o[(ty * kRI + r) * kTile + tx + kTX * c] =
               kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
-    } else {
+    } else if (!idle) {
       double* out = t.prob ? a.out2 : a.out;
       const int64_t ld = t.prob ? a.n_cols : a.ld_out;
       const int64_t n_rows = t.prob ? a.n_rows2 : a.n_rows;
+      const int64_t i0 = bi * kTile - (t.prob ? a.pad_rows2 : a.pad_rows);
+      const int64_t j0 = bj * kTile - (gram ? a.pad_rows : a.pad_cols);
 #pragma unroll
       for (int r = 0; r < kRI; ++r) {
-        const int64_t i = bi * kTile + ty + kTY * r;
+        const int64_t i = i0 + ty * kRI + r;
 #pragma unroll
         for (int c = 0; c < kRJ; ++c) {
-          const int64_t j = bj * kTile + tx + kTX * c;
+          const int64_t j = j0 + tx + kTX * c;
           const double v = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
           if (gram) {
-            if (i < n_rows && j < n_rows) {
+            if (i >= 0 && i < n_rows && j < n_rows) {
               if (i < j) {
                 out[i * ld + j] = v;
                 out[j * ld + i] = v;
@@ -562,7 +576,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
               }
             }
           } else {
-            if (i < n_rows && j < a.n_cols) out[i * ld + j] = v;
+            if (i >= 0 && j >= 0 && i < n_rows && j < a.n_cols) out[i * ld + j] = v;
           }
         }
       }
@@ -607,9 +621,9 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
     if (OUT == QK_OUT_PACKED) {
       a.out[(g - a.tile_begin) * int64_t(kTile * kTile) + il * kTile + jl] = v;
     } else {
-      const int64_t i = bi * kTile + il, j = bj * kTile + jl;
+      const int64_t i = bi * kTile + il - a.pad_rows, j = bj * kTile + jl - a.pad_cols;
       if (MODE == kModeGram) {
-        if (i < a.n_rows && j < a.n_rows) {
+        if (i >= 0 && i < a.n_rows && j < a.n_rows) {
           if (i < j) {
             a.out[i * a.ld_out + j] = v;
             a.out[j * a.ld_out + i] = v;
@@ -617,7 +631,7 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
             a.out[i * a.ld_out + i] = 1.0;
           }
         }
-      } else if (i < a.n_rows && j < a.n_cols) {
+      } else if (i >= 0 && j >= 0 && i < a.n_rows && j < a.n_cols) {
         a.out[i * a.ld_out + j] = v;
       }
     }
@@ -646,8 +660,9 @@ __global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ 
     amp[k] = __longlong_as_double(0x7ff8000000000000LL);
     return;
   }
-  const double2* a = A + (p / kTile) * int64_t(n_pad) * kTile + (p % kTile);
-  const double2* b = B + (q / kTile) * int64_t(n_pad) * kTile + (q % kTile);
+  const int64_t sp = p + sample_pad(n_a), sq = q + sample_pad(n_b);  // plane slots
+  const double2* a = A + (sp / kTile) * int64_t(n_pad) * kTile + (sp % kTile);
+  const double2* b = B + (sq / kTile) * int64_t(n_pad) * kTile + (sq % kTile);
   St s;
   st_init<LAYERS>(s);
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -678,12 +693,13 @@ __global__ void __launch_bounds__(256) unpack_kernel(const double* __restrict__ 
     decode_rect(g, nb_rows, nb_cols, bi, bj);
   }
   const double* src = packed + int64_t(blockIdx.x) * kTile * kTile;
+  const int pr = sample_pad(n_rows), pc = sample_pad(n_cols);
   for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
     const int il = e / kTile, jl = e % kTile;
-    const int64_t i = bi * kTile + il, j = bj * kTile + jl;
+    const int64_t i = bi * kTile + il - pr, j = bj * kTile + jl - pc;
     const double v = src[e];
     if (MODE == kModeGram) {
-      if (i < n_rows && j < n_rows) {
+      if (i >= 0 && i < n_rows && j < n_rows) {
         if (i < j) {
           K[i * ld + j] = v;
           K[j * ld + i] = v;
@@ -691,7 +707,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const double* __restrict__ 
           K[i * ld + i] = 1.0;
         }
       }
-    } else if (i < n_rows && j < n_cols) {
+    } else if (i >= 0 && j >= 0 && i < n_rows && j < n_cols) {
       K[i * ld + j] = v;
     }
   }
@@ -813,6 +829,8 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
   a.n_pad = p.width_padded;
   a.nchunks = p.width_padded / kChunk;
   a.convention = p.convention;
+  a.pad_rows = sample_pad(n_rows);
+  a.pad_cols = sample_pad(n_cols);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool packed = out_mode == QK_OUT_PACKED;
   if (p.layers == 2) {
@@ -876,6 +894,8 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
   a.n_first = n_gram;
   a.out2 = d_K_cross;
   a.progress2 = d_prog_cross;
+  a.pad_rows = a.pad_cols = sample_pad(n_train);
+  a.pad_rows2 = sample_pad(n_test);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (p.layers == 2) return launch_sweep_t<2, kModeJob, QK_OUT_DENSE>(a, st);
   return launch_sweep_t<1, kModeJob, QK_OUT_DENSE>(a, st);
