@@ -1,16 +1,17 @@
 #!/bin/bash
 # Profiling call for the round's profiles/: launch list of the bench command, full ncu captures
-# of the sweep (Gram + cross) and the gate build, and the microbenchmarks.
+# of the joint sweep (config 4) and the gate build, and the microbenchmarks.
 TAG=${1:-r1}
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --e2e-steps 0 \
   --no-cpu-baseline > gpurun_out/launch_bench_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 2 \
-  -o gpurun_out/prof_sweep_$TAG python tools/profile_sweep.py 10000 cross > gpurun_out/ncu_sweep_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 1 \
+  -o gpurun_out/prof_sweep_$TAG python tools/profile_sweep.py > gpurun_out/ncu_sweep_$TAG.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:gate_build -c 1 \
-  -o gpurun_out/prof_gate_$TAG python tools/profile_sweep.py 10000 > gpurun_out/ncu_gate_$TAG.log 2>&1
+  -o gpurun_out/prof_gate_$TAG python tools/profile_sweep.py > gpurun_out/ncu_gate_$TAG.log 2>&1
 ./tools/rfbench > gpurun_out/rfbench_$TAG.txt 2>&1
 ./tools/dmma_bench > gpurun_out/dmma_$TAG.txt 2>&1
+timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 echo done
