@@ -320,11 +320,11 @@ qk_status qk_dfma_peak(double* out_flops_per_s, void* stream) {
 
 // ---- host-buffer pipelines -------------------------------------------------------------
 // H2D of the angles, gate build, ONE persistent sweep launch over every tile, and the D2H of
-// the result overlapped with the sweep: the kernel counts finished tiles per super-row
-// (kGroup tile rows) and a copy stream waits on each counter (cuStreamWaitValue32) before
-// copying that row panel out.  A Gram row is final once its own and all earlier super-rows
-// are done (its lower part mirrors earlier tile rows), and the waits are queued in row
-// order.  Without stream memory operations the D2H follows the sweep.
+// the result overlapped with the sweep: the kernel counts finished tiles per tile row and a
+// copy stream waits on the counters (cuStreamWaitValue32) of a row panel before copying it
+// out.  A Gram row is final once its own and all earlier tile rows are done (its lower part
+// mirrors earlier tile rows), and the waits are queued in row order.  Without stream memory
+// operations the D2H follows the sweep.
 
 }  // extern "C"
 
@@ -353,35 +353,39 @@ struct DrainTarget {
   double* h_K;
   int64_t n_rows, n_cols;
   int mode;              // kModeGram or kModeCross: how tiles map onto super-rows
-  unsigned int* d_prog;  // per-super-row finished-tile counters (set by run_and_drain)
+  unsigned int* d_prog;  // per-tile-row finished-tile counters (set by run_and_drain)
 };
 
 // Resets the progress counters, runs `launch` (which must pass targets[k].d_prog to the
-// sweep) on w->stream, and copies each target's row panels (kGroup tile rows) to the host
+// sweep) on w->stream, and copies each target's row panels (1 or kGroup tile rows) to the host
 // on w->copy_stream as soon as their counters are complete — targets in order, panels in
 // row order, matching the order in which the persistent sweep finishes tiles.
 template <class Launch>
 qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targets,
                         Launch&& launch) {
   StreamWaitValue32Fn wait = stream_wait_value32();
-  int64_t n_super_total = 0;
+  int64_t n_rows_total = 0;  // one counter per tile row
   bool all_pinned = true;
-  size_t panel_bytes = 0;
   for (int k = 0; k < n_targets; ++k) {
-    n_super_total += (blocks_for(tg[k].n_rows) + kGroup - 1) / kGroup;
+    n_rows_total += blocks_for(tg[k].n_rows);
     all_pinned = all_pinned && is_pinned(tg[k].h_K);
-    panel_bytes = std::max(panel_bytes, size_t(kGroup) * kTile * tg[k].n_cols * sizeof(double));
   }
+  // panel height in tile rows: pinned outputs drain per tile row (small tail); pageable ones
+  // per super-row so each staged copy-pool pass moves a few tens of MB
+  const int64_t panel_rows = all_pinned ? 1 : kGroup;
+  size_t panel_bytes = 0;
+  for (int k = 0; k < n_targets; ++k)
+    panel_bytes = std::max(panel_bytes, size_t(panel_rows) * kTile * tg[k].n_cols * 8);
   if (!all_pinned)
     if (qk_status s = w->ensure_stage(panel_bytes)) return s;
   if (wait != nullptr) {
-    if (qk_status s = w->ensure(3, size_t(n_super_total) * sizeof(unsigned int))) return s;
+    if (qk_status s = w->ensure(3, size_t(n_rows_total) * sizeof(unsigned int))) return s;
     unsigned int* base = static_cast<unsigned int*>(w->buf[3]);
-    if (cudaError_t e = cudaMemsetAsync(base, 0, size_t(n_super_total) * 4, w->stream))
+    if (cudaError_t e = cudaMemsetAsync(base, 0, size_t(n_rows_total) * 4, w->stream))
       return cuda_err(e, "progress reset");
     for (int k = 0; k < n_targets; ++k) {
       tg[k].d_prog = base;
-      base += (blocks_for(tg[k].n_rows) + kGroup - 1) / kGroup;
+      base += blocks_for(tg[k].n_rows);
     }
   } else {
     for (int k = 0; k < n_targets; ++k) tg[k].d_prog = nullptr;
@@ -410,17 +414,17 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
     cudaEventDestroy(fin);
   }
   cudaStreamQuery(w->stream);  // flush the launch to the device before host-blocking work
-  // flat list of panels (target, super-row)
+  // flat list of panels (target, panel index); panel sr = tile rows [sr*panel_rows, +panel_rows)
   std::vector<std::pair<int, int64_t>> panels;
   for (int k = 0; k < n_targets; ++k)
-    for (int64_t sr = 0; sr < (blocks_for(tg[k].n_rows) + kGroup - 1) / kGroup; ++sr)
+    for (int64_t sr = 0; sr < (blocks_for(tg[k].n_rows) + panel_rows - 1) / panel_rows; ++sr)
       panels.emplace_back(k, sr);
   const uint32_t unit = p.layers >= 3 ? 16u : 1u;  // L >= 3 counts 16 sub-tiles per tile
   auto rows_of = [&](int k, int64_t sr, int64_t& i0, int64_t& i1) {
-    // sample rows of super-row sr (the front padding of block 0 is not a sample)
+    // sample rows of the panel (the front padding of block 0 is not a sample)
     const int64_t pad = sample_pad(tg[k].n_rows);
-    i0 = std::max<int64_t>(0, sr * kGroup * kTile - pad);
-    i1 = std::min<int64_t>((sr + 1) * kGroup * kTile - pad, tg[k].n_rows);
+    i0 = std::max<int64_t>(0, sr * panel_rows * kTile - pad);
+    i1 = std::min<int64_t>((sr + 1) * panel_rows * kTile - pad, tg[k].n_rows);
   };
   auto enqueue = [&](size_t idx, void* dst) -> cudaError_t {
     const int k = panels[idx].first;
@@ -428,13 +432,12 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
     const DrainTarget& t = tg[k];
     if (t.d_prog != nullptr) {
       const int64_t nbr = blocks_for(t.n_rows), nbc = blocks_for(t.n_cols);
-      const int64_t r0 = sr * kGroup, r1 = std::min<int64_t>(r0 + kGroup, nbr);
-      const uint32_t expect =
-          unit * uint32_t(t.mode == kModeGram
-                              ? upper_row_offset(r1, nbr) - upper_row_offset(r0, nbr)
-                              : (r1 - r0) * nbc);
-      if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + sr), expect, 0x0) != 0)
-        return cudaErrorNotSupported;
+      const int64_t r0 = sr * panel_rows, r1 = std::min<int64_t>(r0 + panel_rows, nbr);
+      for (int64_t r = r0; r < r1; ++r) {  // every tile row of the panel is complete
+        const uint32_t expect = unit * uint32_t(t.mode == kModeGram ? nbr - r : nbc);
+        if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + r), expect, 0x0) != 0)
+          return cudaErrorNotSupported;
+      }
     }
     int64_t i0, i1;
     rows_of(k, sr, i0, i1);

@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       // publish the finished tile to a copy stream waiting on its super-row counter
       __threadfence_system();
       __syncthreads();
-      if (tid == 0) atomicAdd(prog + bi / kGroup, 1u);
+      if (tid == 0) atomicAdd(prog + bi, 1u);  // per tile row
     }
   }
 }
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
     if (a.progress != nullptr) {
       __threadfence_system();
       __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(a.progress + bi / kGroup, 1u);  // 16 per tile
+      if (threadIdx.x == 0) atomicAdd(a.progress + bi, 1u);  // per tile row, 16 per tile
     }
   }
 }
