@@ -194,19 +194,33 @@ class KernelJob:
             mats, handles = None, None
         box = [handles]
         dist.broadcast_object_list(box, src=0, group=self.group)
+        ok = 1.0
         if self.rank != 0:
             shapes = [(lay.n_train, lay.n_train), (lay.n_test, lay.n_train)]
-            mats = [SharedMatrix(r, c, handle=h) for (r, c), h in zip(shapes, box[0])]
+            try:
+                mats = [SharedMatrix(r, c, handle=h) for (r, c), h in zip(shapes, box[0])]
+            except Exception:  # no peer access between these devices
+                mats, ok = [], 0.0
+        # every rank must agree on the placement: fall back to the gather if any import failed
+        flag = torch.tensor([ok], dtype=torch.float64,
+                            device="cpu" if dist.get_backend(self.group) == "gloo" else "cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if flag.item() < 1.0:
+            for m in mats:
+                m.close()
+            self.placement = "gather"
+            return False
         self._shared = mats
         if self.rank == 0:
             self.K_train = mats[0].tensor()
             self.K_cross = mats[1].tensor() if lay.n_test else None
+        return True
 
-    def _run_p2p(self, p_train, p_test):
+    def _run_p2p(self, p_train, p_test, devc):
         from . import device as dev
 
-        if self._shared is None:
-            self._setup_shared()
+        if self._shared is None and not self._setup_shared():
+            return self._run_gather(p_train, p_test, devc)
         lay = self.layout
         lo, hi = lay.union_range(self.rank)  # one launch over this rank's joint tile range
         dev.job_into(p_train, p_test, self._shared[0].ptr,
@@ -264,7 +278,7 @@ class KernelJob:
         if self.world == 1:
             return self._run_local(p_train, p_test, train_angles.device)
         if self.placement == "p2p":
-            return self._run_p2p(p_train, p_test)
+            return self._run_p2p(p_train, p_test, train_angles.device)
         return self._run_gather(p_train, p_test, train_angles.device)
 
     def close(self) -> None:
