@@ -1,0 +1,38 @@
+"""Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck /
+synccheck): gate build, joint sweep (L = 1, 2, 3), dense + packed + unpack, pair kernel,
+host pipelines (pinned and pageable)."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2405_02630_b200 import (FeatureMapConfig, SweepPlan,  # noqa: E402
+                                   compute_kernel_matrices)
+from paper_2405_02630_b200 import device as dev  # noqa: E402
+
+rng = np.random.default_rng(0)
+for L, n in ((2, 40), (1, 20), (3, 6)):
+    Xtr = rng.uniform(0, 1, (150, n))
+    Xte = rng.uniform(0, 1, (70, n))
+    cfg = FeatureMapConfig(n, layers=L)
+    K, Kx = compute_kernel_matrices(Xtr, Xte, cfg)
+    plan = SweepPlan(n, L)
+    pt = dev.gate_build(plan, torch.as_tensor(Xtr, device="cuda"))
+    ps = dev.gate_build(plan, torch.as_tensor(Xte, device="cuda"))
+    nt = plan.gram_tile_count(150)
+    packed = dev.gram(pt, packed=True)
+    Kd = torch.zeros((150, 150), dtype=torch.float64, device="cuda")
+    dev.unpack_gram(plan, packed, 150, 0, nt, Kd)
+    Kxd = dev.cross(ps, pt)
+    pairs = torch.as_tensor(np.array([[0, 1], [5, 149], [149, 0]]), device="cuda")
+    amp = dev.pair_amplitudes(pt, pt, pairs)
+    torch.cuda.synchronize()
+    assert np.array_equal(Kd.cpu().numpy(), K.entries)
+    assert np.array_equal(Kxd.cpu().numpy(), Kx.entries)
+    print("L", L, "ok", float(amp[0]))
+pinned = torch.empty((150, 150), dtype=torch.float64, pin_memory=True).numpy()
+compute_kernel_matrices(rng.uniform(0, 1, (150, 40)), rng.uniform(0, 1, (3, 40)),
+                        FeatureMapConfig(40), out_train=pinned)
+print("sanitize smoke ok")
