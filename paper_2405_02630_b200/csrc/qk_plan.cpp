@@ -64,10 +64,11 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   p.front_pad = p.width_padded - width;
   const int nchunks = p.width_padded / kChunk;
   if (layers == 2) {
-    // The rotated bond-4 recurrence drops a factor 1/2 per qubit (identity qubits included);
-    // the kernel multiplies the state by 2^-512 after every kRescaleChunks chunks.
+    // The rotated bond-4 recurrence drops a factor 1/2 per processed qubit (the identity
+    // qubits of the front padding are skipped, not processed); the kernels multiply the state
+    // by 2^-512 after every kRescaleChunks chunks.
     const int rescales = (nchunks - 1) / kRescaleChunks;
-    p.final_scale = std::ldexp(1.0, -(p.width_padded - 512 * rescales));
+    p.final_scale = std::ldexp(1.0, -(p.width - 512 * rescales));
   } else {
     p.final_scale = 1.0;
   }

@@ -404,7 +404,8 @@ struct SweepArgs {
   int64_t ld_out;
   double final_scale;
   int n_pad, nchunks, convention;
-  unsigned int* progress;  // optional: per-super-row count of finished tiles (host pipelines)
+  int front;               // identity qubits at the front of chunk 0, skipped by the sweep
+  unsigned int* progress;  // optional: per-tile-row count of finished tiles (host pipelines)
   // kModeJob: tiles [0, n_first) are the Gram of (rows = cols); the rest the cross block
   // rows2 x cols (rows2 = test planes) stored to out2 (ld = n_cols), counted in progress2.
   const double2* rows2;
@@ -510,18 +511,24 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       mbar_wait(&full[stage], uint32_t((f / kStages) & 1));
       const double2* sI = sbuf + size_t(stage) * 2 * kChunkElems;
       const double2* sJ = sI + kChunkElems;
+      auto qubit = [&](int q) {
+        double2 vi[kRI], vj[kRJ];
+#pragma unroll
+        for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty * kRI + r];
+#pragma unroll
+        for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
+#pragma unroll
+        for (int r = 0; r < kRI; ++r)
+#pragma unroll
+          for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+      };
       if (!idle) {
+        if (ch == 0 && a.front > 0) {
+          // chunk 0 starts with the identity qubits of the width padding: skip them
+          for (int q = a.front; q < kChunk; ++q) qubit(q);
+        } else {
 #pragma unroll(kQUnroll)
-        for (int q = 0; q < kChunk; ++q) {
-          double2 vi[kRI], vj[kRJ];
-#pragma unroll
-          for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty * kRI + r];
-#pragma unroll
-          for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
-#pragma unroll
-          for (int r = 0; r < kRI; ++r)
-#pragma unroll
-            for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+          for (int q = 0; q < kChunk; ++q) qubit(q);
         }
       }
       __syncwarp();  // every lane's reads of this stage have completed
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
     const double2* pj = a.cols + bj * int64_t(a.n_pad) * kTile + jl;
     St st;
     st_init<LAYERS>(st);
-    for (int q = 0; q < a.n_pad; ++q)
+    for (int q = a.front; q < a.n_pad; ++q)  // the front padding qubits are identities
       st_step<LAYERS>(st, __ldg(pi + int64_t(q) * kTile), __ldg(pj + int64_t(q) * kTile));
     const double v = kernel_value(st_amp<LAYERS>(st, a.final_scale), a.convention);
     if (OUT == QK_OUT_PACKED) {
@@ -651,7 +658,8 @@ __global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ 
                                                     const double2* __restrict__ B, int64_t n_b,
                                                     const int64_t* __restrict__ pairs,
                                                     int64_t n_pairs, double* __restrict__ amp,
-                                                    int n_pad, int nchunks, double final_scale) {
+                                                    int n_pad, int nchunks, int front,
+                                                    double final_scale) {
   using St = typename BondT<LAYERS>::type;
   const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n_pairs) return;
@@ -667,7 +675,7 @@ __global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ 
   st_init<LAYERS>(s);
   for (int ch = 0; ch < nchunks; ++ch) {
 #pragma unroll 4
-    for (int qq = 0; qq < kChunk; ++qq) {
+    for (int qq = ch == 0 ? front : 0; qq < kChunk; ++qq) {  // front padding: identities
       const int64_t off = int64_t(ch * kChunk + qq) * kTile;
       st_step<LAYERS>(s, __ldg(a + off), __ldg(b + off));
     }
@@ -828,6 +836,7 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
   a.final_scale = p.final_scale;
   a.n_pad = p.width_padded;
   a.nchunks = p.width_padded / kChunk;
+  a.front = p.front_pad;
   a.convention = p.convention;
   a.pad_rows = sample_pad(n_rows);
   a.pad_cols = sample_pad(n_cols);
@@ -886,6 +895,7 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
   a.final_scale = p.final_scale;
   a.n_pad = p.width_padded;
   a.nchunks = p.width_padded / kChunk;
+  a.front = p.front_pad;
   a.convention = p.convention;
   a.progress = d_prog_train;
   a.rows2 = static_cast<const double2*>(d_test);
@@ -926,15 +936,18 @@ qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* 
   if (p.layers == 2)
     pairs_kernel<2><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
-                                          n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
+                                          p.final_scale);
   else if (p.layers == 3)
     pairs_kernel<3><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
-                                          n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
+                                          p.final_scale);
   else
     pairs_kernel<1><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
-                                          n_pairs, d_amp, p.width_padded, nchunks, p.final_scale);
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
+                                          p.final_scale);
   return cuda_status(cudaGetLastError(), "pairs launch");
 }
 
