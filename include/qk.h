@@ -71,9 +71,12 @@ typedef struct {
   int64_t reference_cmacs_per_entry;   /* reference planner cost (1056 n - 3912 at L = 2), report only */
 } qk_plan_info;
 
-/* ---- version / errors ---------------------------------------------------- */
+/* ---- version / errors / device ------------------------------------------- */
 int qk_abi_version(void);
 const char* qk_last_error(void);
+/* Make `device` current for libqk's calls on this host thread (one process may drive
+ * several GPUs; launches must run on the device that owns the caller's stream and buffers). */
+qk_status qk_set_device(int32_t device);
 
 /* ---- planner: replaces plan_contraction (paths.py:529-543) + simplify (network.py:183)
  * Fixes the contraction (a qubit-chain sweep with the bond state in registers) once per

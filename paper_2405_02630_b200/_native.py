@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import re
+import threading
 from pathlib import Path
 
 from .errors import CapacityError, DeviceError, NativeLibraryError, RebindError, StructuralError
@@ -42,6 +43,7 @@ class PlanInfo(ctypes.Structure):
 _SIGNATURES = {
     "qk_abi_version": (ctypes.c_int, []),
     "qk_last_error": (ctypes.c_char_p, []),
+    "qk_set_device": (ctypes.c_int, [_c_i32]),
     "qk_plan_create": (ctypes.c_int, [_c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_vp)]),
     "qk_plan_destroy": (ctypes.c_int, [_c_vp]),
     "qk_plan_get_info": (ctypes.c_int, [_c_vp, ctypes.POINTER(PlanInfo)]),
@@ -105,6 +107,24 @@ def lib() -> ctypes.CDLL:
         raise NativeLibraryError("libqk ABI version mismatch")
     _lib = handle
     return _lib
+
+
+_bound = threading.local()
+
+
+def bind_current_device() -> None:
+    """Point libqk's CUDA runtime (linked statically) at the device torch considers current on
+    this thread, so multi-GPU processes launch on the device that owns their streams."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return
+    if not torch.cuda.is_available():
+        return
+    dev = torch.cuda.current_device()
+    if getattr(_bound, "device", None) != dev:
+        check(lib().qk_set_device(dev))
+        _bound.device = dev
 
 
 def last_error() -> str:

@@ -218,6 +218,10 @@ qk_status upload(Workspace* w, void* dst, const void* src, size_t bytes) {
 
 extern "C" {
 
+qk_status qk_set_device(int32_t device) {
+  return cuda_err(cudaSetDevice(device), "cudaSetDevice");
+}
+
 qk_status qk_gate_build(const qk_plan* plan, const double* d_angles, int64_t n_samples,
                         int64_t ld, void* d_planes, uint64_t* d_bad_sample, void* stream) {
   const Plan* p;

@@ -14,6 +14,7 @@ from .planner import SweepPlan
 
 
 def _stream() -> int:
+    _native.bind_current_device()
     return torch.cuda.current_stream().cuda_stream
 
 

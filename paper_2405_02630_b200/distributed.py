@@ -113,6 +113,7 @@ class SharedMatrix:
         self.rows, self.cols = int(rows), int(cols)
         self.owner = handle is None
         lib = _native.lib()
+        _native.bind_current_device()
         p = ctypes.c_void_p()
         if self.owner:
             _native.check(lib.qk_shared_alloc(max(1, self.rows * self.cols) * 8,

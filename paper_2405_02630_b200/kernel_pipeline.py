@@ -237,6 +237,7 @@ def compute_kernel_matrix(features, cfg, plan=None, workers: int = 1, *,
     if N == 1:
         out[0, 0] = 1.0
     elif N >= 2:
+        _native.bind_current_device()
         status = _native.lib().qk_kernel_matrix_host(sp.handle, X.ctypes.data, N,
                                                      out.ctypes.data)
         if status == _native.QK_ERR_REBIND:
@@ -268,6 +269,7 @@ def compute_cross_kernel(test, train, cfg, plan=None, workers: int = 1, *,
     elif out.shape != (Nt, Nr) or out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError(f"out must be a C-contiguous float64 array of shape ({Nt}, {Nr})")
     if Nt and Nr:
+        _native.bind_current_device()
         status = _native.lib().qk_cross_kernel_host(sp.handle, T.ctypes.data, Nt,
                                                      R.ctypes.data, Nr, out.ctypes.data)
         if status == _native.QK_ERR_REBIND:
@@ -305,6 +307,7 @@ def compute_kernel_matrices(train, test, cfg, plan=None, workers: int = 1, *,
     if Nr == 1:
         K[0, 0] = 1.0
     if Nr >= 2 or (Nr and Nt):
+        _native.bind_current_device()
         status = _native.lib().qk_kernel_matrices_host(sp.handle, R.ctypes.data, Nr,
                                                        T.ctypes.data, Nt, K.ctypes.data,
                                                        Kx.ctypes.data)
