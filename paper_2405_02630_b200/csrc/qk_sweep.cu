@@ -424,7 +424,7 @@ struct TileXY {
 template <int LAYERS, int MODE, int OUT, int RI>
 __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
   using St = typename BondT<LAYERS>::type;
-  constexpr int kRI = Geo<RI>::kRI, kTY = Geo<RI>::kTY, kWarps = Geo<RI>::kWarps;
+  constexpr int kRI = Geo<RI>::kRI, kWarps = Geo<RI>::kWarps;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sbuf = reinterpret_cast<double2*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(kStages) * 2 * kChunkBytes);
