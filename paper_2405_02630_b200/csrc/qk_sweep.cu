@@ -49,8 +49,9 @@ constexpr uint32_t kChunkBytes = kChunkElems * 16;     // 16 KB
 // 2 -> 1.212, 4 -> 1.222, 8 -> 1.233, 16 -> 1.215 G entries/s)
 constexpr int kQUnroll = QK_QUNROLL;
 constexpr int kTileTable = 512;  // per-CTA decoded tile coordinates cached in shared memory
-constexpr size_t kSmemBytes =
-    size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8 + kTileTable * 8;  // ring, barriers, table
+constexpr size_t kSmemBytes =  // ring, barriers + release counters, tile table, epilogue stage
+    size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8 + kTileTable * 8 +
+    size_t(kTile) * (kTile + 1) * 8;
 
 static_assert(kRJ * kTX == kTile, "tile mapping");
 
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   const int64_t F = my_tiles * nchunks;
 
   int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
+  double* stage_T = reinterpret_cast<double*>(table + kTileTable);  // epilogue staging tile
   auto decode = [&](int64_t k) -> TileXY {
     const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
     TileXY t;
@@ -560,31 +562,38 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         for (int c = 0; c < kRJ; ++c)
           o[(ty * kRI + r) * kTile + tx + kTX * c] =
               kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
-    } else if (!idle) {
+    } else {
+      // Stage the tile in shared memory, then store it row by row and (Gram) its mirror
+      // column by column, so every store instruction writes whole contiguous rows of K
+      // (full 128 B lines in L2, or over NVLink when K lives on another GPU).
+      __syncthreads();  // the previous tile's store pass has finished reading the stage
+#pragma unroll
+      for (int r = 0; r < kRI; ++r)
+#pragma unroll
+        for (int c = 0; c < kRJ; ++c)
+          stage_T[(ty * kRI + r) * (kTile + 1) + tx + kTX * c] =
+              kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
+      __syncthreads();
       double* out = t.prob ? a.out2 : a.out;
       const int64_t ld = t.prob ? a.n_cols : a.ld_out;
       const int64_t n_rows = t.prob ? a.n_rows2 : a.n_rows;
       const int64_t i0 = bi * kTile - (t.prob ? a.pad_rows2 : a.pad_rows);
       const int64_t j0 = bj * kTile - (gram ? a.pad_rows : a.pad_cols);
-#pragma unroll
-      for (int r = 0; r < kRI; ++r) {
-        const int64_t i = i0 + ty * kRI + r;
-#pragma unroll
-        for (int c = 0; c < kRJ; ++c) {
-          const int64_t j = j0 + tx + kTX * c;
-          const double v = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
-          if (gram) {
-            if (i >= 0 && i < n_rows && j < n_rows) {
-              if (i < j) {
-                out[i * ld + j] = v;
-                out[j * ld + i] = v;
-              } else if (i == j) {
-                out[i * ld + i] = 1.0;
-              }
-            }
-          } else {
-            if (i >= 0 && j >= 0 && i < n_rows && j < a.n_cols) out[i * ld + j] = v;
-          }
+      for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+        const int il = e / kTile, jl = e % kTile;  // consecutive threads: consecutive columns
+        const int64_t i = i0 + il, j = j0 + jl;
+        if (gram) {
+          if (i >= 0 && i < n_rows && j < n_rows && i <= j)
+            out[i * ld + j] = i == j ? 1.0 : stage_T[il * (kTile + 1) + jl];
+        } else if (i >= 0 && j >= 0 && i < n_rows && j < a.n_cols) {
+          out[i * ld + j] = stage_T[il * (kTile + 1) + jl];
+        }
+      }
+      if (gram) {
+        for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+          const int jl = e / kTile, il = e % kTile;  // mirror: row j of K, consecutive i
+          const int64_t i = i0 + il, j = j0 + jl;
+          if (i >= 0 && i < j && j < n_rows) out[j * ld + i] = stage_T[il * (kTile + 1) + jl];
         }
       }
     }
