@@ -8,6 +8,8 @@
 #include <functional>
 #include <thread>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -364,9 +366,34 @@ struct DrainTarget {
 // sweep) on w->stream, and copies each target's row panels (1 or kGroup tile rows) to the host
 // on w->copy_stream as soon as their counters are complete — targets in order, panels in
 // row order, matching the order in which the persistent sweep finishes tiles.
+// QK_TRACE=1: timestamps of the host pipelines' phases on stderr (diagnostics only).
+struct Trace {
+  cudaEvent_t ev[6] = {};
+  bool on = false;
+  explicit Trace(cudaStream_t st) {
+    const char* v = getenv("QK_TRACE");
+    on = v != nullptr && v[0] == '1';
+    if (!on) return;
+    for (auto& e : ev) cudaEventCreate(&e);
+    mark(0, st);
+  }
+  void mark(int k, cudaStream_t st) {
+    if (on) cudaEventRecord(ev[k], st);
+  }
+  ~Trace() {
+    if (!on) return;
+    cudaEventSynchronize(ev[5]);
+    float t[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
+    fprintf(stderr, "qk_trace h2d %.3f gate %.3f sweep %.3f tail %.3f host %.3f ms\n", t[0],
+            t[1], t[2], t[3], t[4]);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
 template <class Launch>
 qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targets,
-                        Launch&& launch) {
+                        Launch&& launch, Trace* trace = nullptr) {
   StreamWaitValue32Fn wait = stream_wait_value32();
   int64_t n_rows_total = 0;  // one counter per tile row
   bool all_pinned = true;
@@ -399,10 +426,12 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   cudaEvent_t reset;
   cudaEventCreateWithFlags(&reset, cudaEventDisableTiming);
   cudaEventRecord(reset, w->stream);
+  if (trace) trace->mark(2, w->stream);
   if (qk_status s = launch()) {
     cudaEventDestroy(reset);
     return s;
   }
+  if (trace) trace->mark(3, w->stream);
   cudaStream_t cs = w->copy_stream;
   if (!all_pinned) {  // the staging slots may still feed the H2D of the inputs
     for (int k = 0; k < 2; ++k)
@@ -478,8 +507,10 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
       }
     }
   }
+  if (trace) trace->mark(4, cs);
   cudaError_t e2 = cudaStreamSynchronize(w->stream);
   cudaError_t e3 = cudaStreamSynchronize(cs);
+  if (trace) trace->mark(5, cs);
   cudaEventDestroy(reset);
   if (e == cudaSuccess) e = e2;
   if (e == cudaSuccess) e = e3;
@@ -591,8 +622,10 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
   double* dKt = static_cast<double*>(w->buf[2]);
   double* dKs = dKt + size_t(n_train) * size_t(n_train);
   cudaStream_t st = w->stream;
+  Trace trace(st);
   if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
   if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
+  trace.mark(1, st);
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
@@ -603,7 +636,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
   if (qk_status s = run_and_drain(w, *p, tg, n_test > 0 ? 2 : 1, [&] {
         return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
                           tg[1].d_prog);
-      }))
+      }, &trace))
     return s;
   static const char* const names[2] = {"train", "test"};
   return check_bad(w->bad, 2, names);

@@ -14,6 +14,10 @@ constexpr int kChunk = 16;   // qubits per bulk-copy chunk Q
 constexpr int kStages = 4;   // shared-memory ring depth
 constexpr int kRescaleChunks = 32;  // L=2: multiply the bond state by 2^-512 every 512 qubits
 constexpr int kGroup = 8;           // tile rows per super-row of the L2-friendly tile order
+#ifndef QK_RECT_GROUP
+#define QK_RECT_GROUP 1
+#endif
+constexpr int kRectGroup = QK_RECT_GROUP;  // tile rows per super-row of cross tile lists
 
 struct Plan {
   int32_t width = 0;

@@ -304,13 +304,22 @@ __device__ __forceinline__ double kernel_value(double amp, int convention) {
   return convention == QK_MAGNITUDE ? fabs(amp) : amp * amp;
 }
 
-// Tile order.  Tiles are grouped into super-rows of kGroup tile rows (the Gram's upper
-// triangle: rows b..nb-1 of each tile row b; the cross rectangle: all nb_cols) and, inside a
-// super-row, walked column by column.  A wave of 148 persistent CTAs then covers ~kGroup tile
-// rows x ~148/kGroup tile columns, whose gate planes (~20 MB at 784 qubits) stay in L2 instead
-// of streaming the whole plane array per wave.  A super-row holds exactly the tiles of its
+// Fence between a tile's stores and its progress-counter bump (host pipelines only).  The
+// tile, the counter and the copy engine's reads all live in / go through this device's memory
+// and L2, so gpu scope suffices; a system-scope fence cost ~3 % of the sweep (measured).
+#ifndef QK_PROGRESS_FENCE
+#define QK_PROGRESS_FENCE __threadfence
+#endif
+
+// Tile order.  Gram tiles are grouped into super-rows of kGroup tile rows (rows b..nb-1 of
+// each tile row b of the upper triangle) and, inside a super-row, walked column by column: a
+// wave of 148 persistent CTAs then covers ~kGroup tile rows x ~148/kGroup tile columns, whose
+// gate planes (~20 MB at 784 qubits) stay in L2.  A super-row holds exactly the tiles of its
 // rows, so super-row boundaries coincide with plain row-major offsets (used by the host-side
-// row panels).
+// row panels).  Cross tiles use kRectGroup (1 = row-major): a wave then finishes about one
+// tile row, so the host pipeline's D2H tail after the sweep is one 64-row panel (0.1 ms at
+// config 4) instead of a whole super-row (0.6 ms); the extra plane re-reads are L2/DRAM
+// traffic the FP64-bound sweep does not notice (measured).
 // Row-major position -> tile row (the plain upper-triangle row containing linear index g).
 __host__ __device__ __forceinline__ int64_t upper_row_of(int64_t g, int64_t nb) {
   const double m = 2.0 * double(nb) + 1.0;
@@ -342,8 +351,8 @@ __host__ __device__ __forceinline__ void decode_upper(int64_t g, int64_t nb, int
 
 __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows, int64_t nb_cols,
                                             int64_t& bi, int64_t& bj) {
-  const int64_t r0 = (g / (kGroup * nb_cols)) * kGroup;
-  const int64_t h = nb_rows - r0 < kGroup ? nb_rows - r0 : kGroup;
+  const int64_t r0 = (g / (kRectGroup * nb_cols)) * kRectGroup;
+  const int64_t h = nb_rows - r0 < kRectGroup ? nb_rows - r0 : kRectGroup;
   const int64_t local = g - r0 * nb_cols;
   bj = local / h;
   bi = r0 + local % h;
@@ -600,7 +609,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     unsigned int* prog = t.prob ? a.progress2 : a.progress;
     if (prog != nullptr) {
       // publish the finished tile to a copy stream waiting on its super-row counter
-      __threadfence_system();
+      QK_PROGRESS_FENCE();
       __syncthreads();
       if (tid == 0) atomicAdd(prog + bi, 1u);  // per tile row
     }
@@ -652,7 +661,7 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
       }
     }
     if (a.progress != nullptr) {
-      __threadfence_system();
+      QK_PROGRESS_FENCE();
       __syncthreads();
       if (threadIdx.x == 0) atomicAdd(a.progress + bi, 1u);  // per tile row, 16 per tile
     }
