@@ -481,10 +481,46 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   cudaError_t e = cudaSuccess;
   const size_t np = panels.size();
   if (all_pinned) {
-    for (size_t idx = 0; idx < np && e == cudaSuccess; ++idx) {
-      int64_t i0, i1;
-      rows_of(panels[idx].first, panels[idx].second, i0, i1);
-      e = enqueue(idx, tg[panels[idx].first].h_K + i0 * tg[panels[idx].first].n_cols);
+    // Per tile row, straight into the user's pinned matrix.  A Gram row panel q is split: its
+    // columns of blocks < q-kLag+1 are mirrors of tiles in tile rows <= q-kLag, so they go out
+    // right after THAT row's wait; only the rest waits for row q.  The last tile rows finish
+    // together in the sweep's final wave, and this leaves just their upper parts (a few MB)
+    // after it instead of whole 64 x n panels.
+    constexpr int64_t kLag = 2 * kGroup;
+    for (int k = 0; k < n_targets && e == cudaSuccess; ++k) {
+      const DrainTarget& t = tg[k];
+      const int64_t nbr = blocks_for(t.n_rows);
+      const int64_t pad_r = sample_pad(t.n_rows), pad_c = sample_pad(t.n_cols);
+      auto row_lo = [&](int64_t b) {
+        return std::min(std::max<int64_t>(b * kTile - pad_r, 0), t.n_rows);
+      };
+      auto col_lo = [&](int64_t b) {
+        return std::min(std::max<int64_t>(b * kTile - pad_c, 0), t.n_cols);
+      };
+      auto copy = [&](int64_t r, int64_t c0, int64_t c1) -> cudaError_t {
+        const int64_t i0 = row_lo(r), i1 = row_lo(r + 1);
+        if (i1 <= i0 || c1 <= c0) return cudaSuccess;
+        const size_t pitch = size_t(t.n_cols) * sizeof(double);
+        return cudaMemcpy2DAsync(t.h_K + i0 * t.n_cols + c0, pitch, t.d_K + i0 * t.n_cols + c0,
+                                 pitch, size_t(c1 - c0) * sizeof(double), size_t(i1 - i0),
+                                 cudaMemcpyDeviceToHost, cs);
+      };
+      const bool split = t.mode == kModeGram && t.d_prog != nullptr;
+      for (int64_t q = 0; q < nbr && e == cudaSuccess; ++q) {
+        if (t.d_prog != nullptr) {
+          const uint32_t expect =
+              unit * uint32_t(t.mode == kModeGram ? nbr - q : blocks_for(t.n_cols));
+          if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + q), expect, 0x0) != 0)
+            e = cudaErrorNotSupported;
+        }
+        if (e != cudaSuccess) break;
+        if (!split) {
+          e = copy(q, 0, t.n_cols);
+          continue;
+        }
+        e = copy(q, col_lo(std::max<int64_t>(0, q - kLag + 1)), t.n_cols);
+        if (e == cudaSuccess && q + kLag < nbr) e = copy(q + kLag, 0, col_lo(q + 1));
+      }
     }
   } else {
     // two pinned slots: DMA panel idx+2 while the pool copies panel idx into the user buffer
@@ -538,7 +574,9 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
   if (qk_status s = w->ensure(2, size_t(N) * size_t(N) * sizeof(double))) return s;
   double* dX = static_cast<double*>(w->buf[0]);
   cudaStream_t st = w->stream;
+  Trace trace(st);
   if (qk_status s = upload(w, dX, h_angles, xb)) return s;
+  trace.mark(1, st);
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
@@ -548,7 +586,7 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
         return launch_sweep(*p, kModeGram, planes, N, planes, N, 0,
                             qk_gram_tile_count(plan, N), tg[0].d_K, N, QK_OUT_DENSE, w->stream,
                             tg[0].d_prog);
-      }))
+      }, &trace))
     return s;
   static const char* const names[1] = {"train"};
   return check_bad(w->bad, 1, names);
@@ -576,8 +614,10 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   char* dPr = static_cast<char*>(w->buf[1]);
   char* dPc = dPr + prb;
   cudaStream_t st = w->stream;
+  Trace trace(st);
   if (qk_status s = upload(w, dXr, h_rows, xrb)) return s;
   if (qk_status s = upload(w, dXc, h_cols, xcb)) return s;
+  trace.mark(1, st);
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
   if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
@@ -588,7 +628,7 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
         return launch_sweep(*p, kModeCross, dPr, n_rows, dPc, n_cols, 0,
                             qk_cross_tile_count(plan, n_rows, n_cols), tg[0].d_K, n_cols,
                             QK_OUT_DENSE, w->stream, tg[0].d_prog);
-      }))
+      }, &trace))
     return s;
   static const char* const names[2] = {"test", "train"};
   return check_bad(w->bad, 2, names);

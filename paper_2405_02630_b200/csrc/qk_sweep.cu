@@ -166,6 +166,81 @@ __device__ __forceinline__ void bond4_step(Bond4& s, double2 vi, double2 vj) {
   s.tm = ntm;
 }
 
+// Whole-micro-tile step in an explicit issue order (QK_MT = 1: plain C++, 2: each FP64 op an
+// asm volatile statement so ptxas sees them in this order).  Same operations and operands as
+// bond4_step (STEPV 2) up to commuted multiplicands, so bit-identical.  Order: per tile row,
+// c and d of all its pairs back to back (b_i stays in slot A: operand-reuse cache), then per
+// pair the state update with the T+ pair and the T- pair of DFMAs adjacent (shared slot A).
+#ifndef QK_MT
+#define QK_MT 0
+#endif
+#if QK_MT == 2
+__device__ __forceinline__ double xfma(double a, double b, double c) {
+  double d;
+  asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(d) : "d"(a), "d"(b), "d"(c));
+  return d;
+}
+__device__ __forceinline__ double xmul(double a, double b) {
+  double d;
+  asm volatile("mul.rn.f64 %0, %1, %2;" : "=d"(d) : "d"(a), "d"(b));
+  return d;
+}
+__device__ __forceinline__ double xadd(double a, double b) {
+  double d;
+  asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(d) : "d"(a), "d"(b));
+  return d;
+}
+__device__ __forceinline__ double xsub(double a, double b) {
+  double d;
+  asm volatile("sub.rn.f64 %0, %1, %2;" : "=d"(d) : "d"(a), "d"(b));
+  return d;
+}
+#else
+__device__ __forceinline__ double xfma(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+#endif
+
+template <int NI, int NJ>
+__device__ __forceinline__ void bond4_tile_step(Bond4 (&st)[NI][NJ], const double2 (&vi)[NI],
+                                                const double2 (&vj)[NJ]) {
+  double c[NI][NJ], d[NI][NJ];
+#pragma unroll
+  for (int r = 0; r < NI; ++r) {
+    double p[NJ], q[NJ];
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) p[k] = xmul(vi[r].x, vj[k].x);
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) q[k] = xmul(vi[r].x, vj[k].y);
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+      c[r][k] = xfma(vi[r].y, vj[k].y, p[k]);
+      d[r][k] = xfma(-vi[r].y, vj[k].x, q[k]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NI; ++r)
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+      const double ai = vi[r].x, bi = vi[r].y, aj = vj[k].x, bj = vj[k].y;
+      Bond4& s = st[r][k];
+      const double s1 = xadd(bi, bj), d2 = xsub(bi, bj), s2 = xadd(ai, aj), d1 = xsub(aj, ai);
+      const double x = xfma(c[r][k], s.sp, s.sp);
+      const double y = xmul(d1, s.sp);
+      const double z = xmul(s2, s.sm);
+      const double w = xfma(c[r][k], s.sm, -s.sm);
+      const double nsp = xfma(s.tp, s1, x);
+      const double ntm = xfma(s.tp, -d[r][k], y);
+      const double nsm = xfma(s.tm, d[r][k], z);
+      const double ntp = xfma(s.tm, d2, w);
+      s.sp = nsp;
+      s.tp = ntp;
+      s.sm = nsm;
+      s.tm = ntm;
+    }
+}
+
 __device__ __forceinline__ void bond4_scale(Bond4& s, double f) {
   s.sp *= f;
   s.tp *= f;
@@ -528,10 +603,14 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty * kRI + r];
 #pragma unroll
         for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
+        if constexpr (LAYERS == 2 && QK_MT != 0) {
+          bond4_tile_step<kRI, kRJ>(st, vi, vj);
+        } else {
 #pragma unroll
-        for (int r = 0; r < kRI; ++r)
+          for (int r = 0; r < kRI; ++r)
 #pragma unroll
-          for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+            for (int c = 0; c < kRJ; ++c) st_step<LAYERS>(st[r][c], vi[r], vj[c]);
+        }
       };
       if (!idle) {
         if (ch == 0 && a.front > 0) {

@@ -196,6 +196,11 @@ def test_full_size_gram_properties_and_sampled_parity():
     assert np.abs(K[i[keep], j[keep]] - ref).max() <= K_ABS
     med = np.median(ref)
     assert 1e-3 <= med <= 0.5  # parity data is not in the concentrated K ~ 0 regime
+    # the pinned-output pipeline (per-tile-row D2H racing the sweep, Gram panels split at
+    # full size) lands the same bits as the pageable one
+    pinned = torch.empty((10000, 10000), dtype=torch.float64, pin_memory=True).numpy()
+    pinned.fill(np.nan)
+    assert np.array_equal(compute_kernel_matrix(Atr, cfg, out=pinned).entries, K)
 
 
 def test_svc_predictions_identical(rng):

@@ -25,7 +25,7 @@ def parse(ins):
     ops = [o.strip() for o in rest.split(",")] if rest else []
     return op, ops
 
-# hot loop = the backward branch target range with the most DP instructions
+# hot loop = the backward-branch range with the highest DP density
 dp = lambda op: op.split(".")[0] in ("DFMA", "DMUL", "DADD")
 best = None
 for k, ins in enumerate(lines):
@@ -41,9 +41,12 @@ for k, ins in enumerate(lines):
             j = addrs.index(tgt)
             if j < k:
                 n = sum(1 for x in lines[j:k + 1] if dp(parse(x)[0]))
-                if best is None or n > best[2]:
-                    best = (j, k, n)
-j, k, n = best
+                dens = n / (k + 1 - j)
+                # the hot loop: the densest loop of DP instructions (an outer loop that
+                # contains it has more DP instructions but a lower density)
+                if n >= 64 and (best is None or dens > best[3]):
+                    best = (j, k, n, dens)
+j, k, n, _ = best
 loop = lines[j:k + 1]
 prev = [None, None, None]
 cycles = 0
