@@ -171,6 +171,25 @@ qk_status qk_ipc_export(const void* d_ptr, unsigned char out_handle[QK_IPC_HANDL
 qk_status qk_ipc_import(const unsigned char handle[QK_IPC_HANDLE_BYTES], void** out_d_ptr);
 qk_status qk_ipc_close(void* d_ptr);
 
+/* ---- dense state-vector ground truth (checker beyond the reference's 24-qubit guard) ----
+ * Replaces the reference's brute-force simulator (statevector.py:41-70, simulate /
+ * zero_amplitude / kernel_entry_oracle) for the pair circuit compose_kernel_circuit(x_i, x_j)
+ * (circuit.py:150-157): every gate in the reference's order on a real fp64 state, amplitudes
+ * bit-identical to the reference's complex128 simulate().  Independent of the sweep.
+ *   qk_statevector_amplitude: one pair, host angle vectors x_i, x_j [width]; d_state is a
+ *     caller-owned device buffer of qk_statevector_bytes(width) bytes; *out_amp (host) gets
+ *     <0..0| U(x_i)^dag U(x_j) |0..0>.  Width <= 40 (memory permitting).
+ *   qk_statevector_pairs: many pairs at width <= 13 (state in shared memory, one CTA per
+ *     pair); host angle sets A [n_a x width], B [n_b x width], 0-based pairs (row of A,
+ *     row of B), host amplitudes out.  Synchronous. */
+size_t qk_statevector_bytes(int32_t width);
+qk_status qk_statevector_amplitude(int32_t width, int32_t layers, const double* x_i,
+                                   const double* x_j, double* d_state, double* out_amp,
+                                   void* stream);
+qk_status qk_statevector_pairs(int32_t width, int32_t layers, const double* h_a, int64_t n_a,
+                               const double* h_b, int64_t n_b, const int64_t* h_pairs,
+                               int64_t n_pairs, double* h_amp);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "_lib" / "libqk.so"
-SOURCES = ["qk_plan.cpp", "qk_sweep.cu", "qk_api.cu"]
+SOURCES = ["qk_plan.cpp", "qk_sweep.cu", "qk_api.cu", "qk_statevector.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

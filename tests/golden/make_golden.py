@@ -3,7 +3,8 @@
 Run in the build container only (it imports /root/reference/pkg/src/tnkernel, which does
 not exist on the GPU box):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py        # the contract_batch cases + known answers
+    python tests/golden/make_golden.py sv     # the state-vector cases (sv_*.npz)
 
 Each case stores the angles, the pair list and the reference amplitudes returned by
 ``contract_batch(template, pairs, plan_contraction(template), workers)``
@@ -114,7 +115,34 @@ def known_answers():
     print("known_answers:", len(rows))
 
 
+def sv_cases():
+    """Reference brute-force amplitudes (statevector.py:57-59 zero_amplitude of
+    compose_kernel_circuit) for the GPU state-vector simulator's bit-identity test."""
+    sys.path.insert(0, str(REF))
+    from tnkernel.circuit import FeatureMapConfig, compose_kernel_circuit
+    from tnkernel.statevector import zero_amplitude
+
+    rng = np.random.default_rng(240502630 + 77)
+    for n, L, n_pairs, spread in [(1, 2, 4, 1.0), (5, 1, 6, 0.8), (5, 2, 8, 0.8),
+                                  (9, 2, 8, 0.4), (12, 3, 4, 0.3), (13, 2, 6, 0.3),
+                                  (16, 2, 3, 0.2), (19, 2, 2, 0.15)]:
+        X = clustered_angles(rng, 6, n, spread)
+        pairs = rng.integers(0, 6, (n_pairs, 2)).astype(np.int64)
+        cfg = FeatureMapConfig(n, layers=L)
+        t0 = time.time()
+        amps = np.array([zero_amplitude(compose_kernel_circuit(X[p], X[q], cfg))
+                         for p, q in pairs], dtype=np.complex128)
+        name = f"sv_n{n}_L{L}"
+        np.savez_compressed(OUT / f"{name}.npz", kind="statevector", layers=L, A=X, B=X,
+                            pairs=pairs, amp_re=amps.real, amp_im=amps.imag)
+        print(f"{name}: {n_pairs} pairs in {time.time() - t0:.1f}s, "
+              f"|amp| range [{np.abs(amps).min():.3g}, {np.abs(amps).max():.3g}]")
+
+
 def main():
+    if sys.argv[1:] == ["sv"]:
+        sv_cases()
+        return
     rng = np.random.default_rng(240502630)
     known_answers()
     gram_case("gram_n8_L2", rng, 24, 8, 2, 0.35)

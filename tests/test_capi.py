@@ -95,3 +95,20 @@ def test_missing_library_is_a_hard_error(tmp_path, monkeypatch):
 
     with pytest.raises(NativeLibraryError, match="no CPU fallback"):
         _native.lib()
+
+
+def test_statevector_entry_points_validate_before_touching_the_device():
+    lib = _native.lib()
+    assert lib.qk_statevector_bytes(30) == 8 << 30 and lib.qk_statevector_bytes(0) == 0
+    A = np.zeros((2, 4))
+    out = np.empty(1)
+    bad = np.array([[0, 2]], dtype=np.int64)
+    assert lib.qk_statevector_pairs(4, 2, A.ctypes.data, 2, A.ctypes.data, 2, bad.ctypes.data,
+                                    1, out.ctypes.data) == _native.QK_ERR_VALUE
+    assert "indexes outside" in _native.last_error()
+    assert lib.qk_statevector_pairs(14, 2, A.ctypes.data, 0, A.ctypes.data, 0, bad.ctypes.data,
+                                    1, out.ctypes.data) == _native.QK_ERR_CAPACITY
+    A[1, 2] = np.inf
+    ok = np.array([[0, 1]], dtype=np.int64)
+    assert lib.qk_statevector_pairs(4, 2, A.ctypes.data, 2, A.ctypes.data, 2, ok.ctypes.data,
+                                    1, out.ctypes.data) == _native.QK_ERR_REBIND
