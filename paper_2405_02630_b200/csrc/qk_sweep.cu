@@ -351,6 +351,10 @@ template <>
 struct BondT<3> {
   using type = BondG<2>;
 };
+template <>
+struct BondT<4> {
+  using type = BondG<3>;
+};
 
 template <int LAYERS>
 __device__ __forceinline__ void st_init(typename BondT<LAYERS>::type& s) {
@@ -382,6 +386,11 @@ __device__ __forceinline__ double kernel_value(double amp, int convention) {
 // Fence between a tile's stores and its progress-counter bump (host pipelines only).  The
 // tile, the counter and the copy engine's reads all live in / go through this device's memory
 // and L2, so gpu scope suffices; a system-scope fence cost ~3 % of the sweep (measured).
+// Sweep epilogue: 0 = CTA-staged whole-row stores (two CTA barriers per tile), 1 = per-warp.
+#ifndef QK_EPI
+#define QK_EPI 0
+#endif
+
 #ifndef QK_PROGRESS_FENCE
 #define QK_PROGRESS_FENCE __threadfence
 #endif
@@ -650,6 +659,55 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         for (int c = 0; c < kRJ; ++c)
           o[(ty * kRI + r) * kTile + tx + kTX * c] =
               kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
+    } else if (QK_EPI == 1) {
+      // Per-warp epilogue, no CTA barrier: the warp's 2*kRI rows go out straight from the
+      // registers (each store instruction writes two 128 B row segments), and the Gram mirror
+      // through a warp-private transposing stage in shared memory (each lane writes the
+      // warp's 2*kRI values of one or two rows of K).
+      constexpr int kWR = 2 * kRI;  // rows per warp
+      double* out = t.prob ? a.out2 : a.out;
+      const int64_t ld = t.prob ? a.n_cols : a.ld_out;
+      const int64_t n_rows = t.prob ? a.n_rows2 : a.n_rows;
+      const int64_t i0 = bi * kTile - (t.prob ? a.pad_rows2 : a.pad_rows);
+      const int64_t j0 = bj * kTile - (gram ? a.pad_rows : a.pad_cols);
+      double v[kRI][kRJ];
+#pragma unroll
+      for (int r = 0; r < kRI; ++r)
+#pragma unroll
+        for (int c = 0; c < kRJ; ++c) {
+          v[r][c] = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
+          const int64_t i = i0 + ty * kRI + r, j = j0 + tx + kTX * c;
+          if (gram) {
+            if (i >= 0 && i < n_rows && j < n_rows && i <= j)
+              out[i * ld + j] = i == j ? 1.0 : v[r][c];
+          } else if (i >= 0 && j >= 0 && i < n_rows && j < a.n_cols) {
+            out[i * ld + j] = v[r][c];
+          }
+        }
+      if (gram) {
+        const int w = tid / 32;
+        double* wb = stage_T + w * (kWR * (kTile + 1));
+        __syncwarp();  // this warp's mirror pass of the previous tile has read wb
+#pragma unroll
+        for (int r = 0; r < kRI; ++r)
+#pragma unroll
+          for (int c = 0; c < kRJ; ++c)
+            wb[((ty & 1) * kRI + r) * (kTile + 1) + tx + kTX * c] = v[r][c];
+        __syncwarp();
+        const int64_t iw = i0 + w * kWR;  // first row of this warp
+#pragma unroll
+        for (int h = 0; h < kTile / 32; ++h) {
+          const int jl = lane + 32 * h;
+          const int64_t j = j0 + jl;
+          if (j < n_rows) {
+#pragma unroll
+            for (int lr = 0; lr < kWR; ++lr) {
+              const int64_t i = iw + lr;
+              if (i >= 0 && i < j) out[j * ld + i] = wb[lr * (kTile + 1) + jl];
+            }
+          }
+        }
+      }
     } else {
       // Stage the tile in shared memory, then store it row by row and (Gram) its mirror
       // column by column, so every store instruction writes whole contiguous rows of K
@@ -953,6 +1011,13 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
     return packed ? launch_sweep_t<1, kModeCross, QK_OUT_PACKED>(a, st)
                   : launch_sweep_t<1, kModeCross, QK_OUT_DENSE>(a, st);
   }
+  if (p.layers == 4) {
+    if (mode == kModeGram)
+      return packed ? launch_general<4, kModeGram, QK_OUT_PACKED>(a, st)
+                    : launch_general<4, kModeGram, QK_OUT_DENSE>(a, st);
+    return packed ? launch_general<4, kModeCross, QK_OUT_PACKED>(a, st)
+                  : launch_general<4, kModeCross, QK_OUT_DENSE>(a, st);
+  }
   if (mode == kModeGram)
     return packed ? launch_general<3, kModeGram, QK_OUT_PACKED>(a, st)
                   : launch_general<3, kModeGram, QK_OUT_DENSE>(a, st);
@@ -967,8 +1032,8 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
   if (tile_end <= tile_begin) return QK_OK;
   const int64_t nbt = blocks_for(n_train);
   const int64_t n_gram = nbt * (nbt + 1) / 2;
-  if (p.layers == 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
-    // one problem only (or the one-pair-per-thread L = 3 kernel): plain launches
+  if (p.layers >= 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
+    // one problem only (or the one-pair-per-thread L >= 3 kernel): plain launches
     if (qk_status s = launch_sweep(p, kModeGram, d_train, n_train, d_train, n_train, tile_begin,
                                    std::min(tile_end, n_gram), d_K_train, n_train,
                                    QK_OUT_DENSE, stream, d_prog_train))
@@ -1037,6 +1102,11 @@ qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* 
                                           p.final_scale);
   else if (p.layers == 3)
     pairs_kernel<3><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
+                                          static_cast<const double2*>(d_b), n_b, d_pairs,
+                                          n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
+                                          p.final_scale);
+  else if (p.layers == 4)
+    pairs_kernel<4><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
                                           n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
                                           p.final_scale);

@@ -5,6 +5,7 @@ not exist on the GPU box):
 
     python tests/golden/make_golden.py        # the contract_batch cases + known answers
     python tests/golden/make_golden.py sv     # the state-vector cases (sv_*.npz)
+    python tests/golden/make_golden.py l4     # layers = 4 cases
 
 Each case stores the angles, the pair list and the reference amplitudes returned by
 ``contract_batch(template, pairs, plan_contraction(template), workers)``
@@ -139,9 +140,19 @@ def sv_cases():
               f"|amp| range [{np.abs(amps).min():.3g}, {np.abs(amps).max():.3g}]")
 
 
+def l4_cases():
+    """layers = 4 (bond-64 transfer): the reference's contract_batch (its planner slices)."""
+    rng = np.random.default_rng(240502630 + 4)
+    gram_case("gram_n5_L4", rng, 8, 5, 4, 0.4)
+    sampled_case("pairs_n24_L4", rng, 10, 24, 4, 0.1, 12)
+
+
 def main():
     if sys.argv[1:] == ["sv"]:
         sv_cases()
+        return
+    if sys.argv[1:] == ["l4"]:
+        l4_cases()
         return
     rng = np.random.default_rng(240502630)
     known_answers()
