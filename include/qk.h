@@ -60,7 +60,7 @@ typedef struct {
   int32_t width;           /* qubits n (= features per sample) */
   int32_t layers;          /* feature-map layers L */
   int32_t convention;      /* qk_convention */
-  int32_t bond;            /* transfer-state size per pair: 4^(L-1) = 1, 4, 16 */
+  int32_t bond;            /* transfer-state size per pair: 4^(L-1) = 1, 4, 16, ..., 16384 */
   int32_t tile_edge;       /* samples per tile edge T (and per plane block) */
   int32_t chunk;           /* qubits per staged chunk Q */
   int32_t width_padded;    /* n rounded up to a multiple of Q (identity qubits in front) */
@@ -82,7 +82,9 @@ qk_status qk_set_device(int32_t device);
  * Fixes the contraction (a qubit-chain sweep with the bond state in registers) once per
  * circuit structure (width, layers, convention); every pair reuses it ("path reuse",
  * SPEC.md:340).  Pure host code: validates like FeatureMapConfig
- * (circuit.py:86-91) and never touches the GPU.  layers must be 1, 2 or 3 (bond 1/4/16). */
+ * (circuit.py:86-91) and never touches the GPU.  layers 1..8: bond 4^(L-1) in registers for
+ * L <= 4, in shared memory for L = 5..8; layers > 8 -> QK_ERR_CAPACITY (the reference's own
+ * contraction of those circuits hits its intermediate cap or runs for hours per entry). */
 qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_plan** out_plan);
 qk_status qk_plan_destroy(qk_plan* plan);
 qk_status qk_plan_get_info(const qk_plan* plan, qk_plan_info* out_info);

@@ -37,7 +37,7 @@
 
 typedef double complex cplx;
 
-#define MAX_LAYERS 5
+#define MAX_LAYERS 8
 
 /* Apply the 2x2 matrix m (row-major) to the wire value of every boundary slot. */
 static void apply_wire(cplx* psi, int nk, const cplx m[4]) {

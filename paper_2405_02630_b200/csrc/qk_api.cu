@@ -452,7 +452,7 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   for (int k = 0; k < n_targets; ++k)
     for (int64_t sr = 0; sr < (blocks_for(tg[k].n_rows) + panel_rows - 1) / panel_rows; ++sr)
       panels.emplace_back(k, sr);
-  const uint32_t unit = p.layers >= 3 ? 16u : 1u;  // L >= 3 counts 16 sub-tiles per tile
+  const uint32_t unit = progress_unit(p.layers);
   auto rows_of = [&](int k, int64_t sr, int64_t& i0, int64_t& i1) {
     // sample rows of the panel (the front padding of block 0 is not a sample)
     const int64_t pad = sample_pad(tg[k].n_rows);

@@ -13,6 +13,7 @@ constexpr int kTile = 64;    // samples per plane block == tile edge T
 constexpr int kChunk = 16;   // qubits per bulk-copy chunk Q
 constexpr int kStages = 4;   // shared-memory ring depth
 constexpr int kRescaleChunks = 32;  // L=2: multiply the bond state by 2^-512 every 512 qubits
+constexpr int kMaxLayers = 8;       // L <= 4: registers; L = 5..8: shared-memory deep sweep
 constexpr int kGroup = 8;           // tile rows per super-row of the L2-friendly tile order
 #ifndef QK_RECT_GROUP
 #define QK_RECT_GROUP 1
@@ -44,6 +45,12 @@ int64_t blocks_for(int64_t n_samples);
 // t of block b holds sample 64 b + t - pad), so it is a tile ROW of every Gram tile that
 // touches it and whole warps of those tiles can skip it.
 QK_HD inline int sample_pad(int64_t n) { return int((kTile - n % kTile) % kTile); }
+
+// Progress-counter increments per finished tile (host pipelines): L <= 2 one per tile, L = 3, 4
+// one per 16x16 sub-tile, L >= 5 one per pair group of the deep sweep (4 pairs at L = 5).
+QK_HD inline uint32_t progress_unit(int layers) {
+  return layers <= 2 ? 1u : layers <= 4 ? 16u : uint32_t(kTile * kTile / (layers == 5 ? 4 : 1));
+}
 
 // First linear index of tile row r in the upper-triangle tile list over nb blocks.
 QK_HD inline int64_t upper_row_offset(int64_t r, int64_t nb) { return r * nb - r * (r - 1) / 2; }

@@ -48,11 +48,12 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   if (layers < 1) return set_error(QK_ERR_VALUE, "layers must be >= 1");
   if (convention != QK_PROBABILITY && convention != QK_MAGNITUDE)
     return set_error(QK_ERR_VALUE, "unknown kernel convention " + std::to_string(convention));
-  if (layers > 4)
+  if (layers > kMaxLayers)
     return set_error(QK_ERR_CAPACITY,
-                     "layers=" + std::to_string(layers) +
-                         " needs a bond-" + std::to_string(1 << (2 * (layers - 1))) +
-                         " transfer state; the sm_100a sweep implements layers 1 to 4");
+                     "layers=" + std::to_string(layers) + " needs a bond-" +
+                         std::to_string(int64_t(1) << (2 * (layers - 1))) +
+                         " transfer state per pair; the sm_100a sweep implements layers 1 to " +
+                         std::to_string(kMaxLayers) + " (shared-memory state <= 128 KB)");
 
   qk_plan* h = new (std::nothrow) qk_plan();
   if (h == nullptr) return set_error(QK_ERR_CAPACITY, "out of host memory");
@@ -97,13 +98,12 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
     in.algorithmic_flops_per_entry = 4 * n;
     in.reference_cmacs_per_entry = 0;
   } else {
-    // L >= 3, bond D = 2^(L-1) per side (V is D x D): per qubit per pair two D x D site
-    // matrices (2 (L-2) D^2 DMUL), F_i^T V and (.)F_j (2 (D^2 DMUL + (D^3 - D^2) DFMA)),
-    // RY(delta) (2 DMUL + 2 DFMA) and the mask (D^2 DMUL); 15 for the final sum and square
-    const int64_t D = int64_t(1) << (layers - 1), D2 = D * D, D3 = D2 * D;
-    const int64_t mul = 2 * (layers - 2) * D2 + 2 * D2 + 2 + D2, fma = 2 * (D3 - D2) + 2;
-    in.dp_instr_per_entry = (mul + fma) * n + 15;
-    in.flops_per_entry = (mul + 2 * fma) * n + 15;
+    // L >= 3, D = 2^(L-1), V is D x D (E = D^2 elements).  Per qubit per pair: two sides of
+    // M = L-1 level passes, each D^2/2 rotations of 2 DMUL + 2 DFMA (6 flops); cos/sin of
+    // delta/2 (2 DMUL + 2 DFMA); the RY(delta) mask (E DMUL).  E - 1 adds and the square last.
+    const int64_t M = layers - 1, E = int64_t(1) << (2 * M);
+    in.dp_instr_per_entry = (4 * M * E + E + 4) * n + E;
+    in.flops_per_entry = (6 * M * E + E + 6) * n + E;
     in.algorithmic_flops_per_entry = in.flops_per_entry;
     in.reference_cmacs_per_entry = 0;
   }

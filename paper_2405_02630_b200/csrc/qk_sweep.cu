@@ -262,78 +262,70 @@ __device__ __forceinline__ void bond1_step(Bond1& s, double2 vi, double2 vj) {
 
 // L >= 3: amp = <phi_{L-1}(x_i)| R(x_j - x_i) |phi_{L-1}(x_j)>, phi_m = (C R)^m |0> is an MPS
 // of bond D = 2^m whose site matrix is F(x)[a][b] = prod_k RY(x)[a_k ^ b_k][b_{k-1}] (level-k
-// bits, b_0 = 0); the pair state V is D x D and one qubit is V <- (F_i^T V F_j) o RY(delta)
+// bits, b_{-1} = 0); the pair state V is D x D and one qubit is V <- (F_i^T V F_j) o RY(delta)
 // on the top-level bits.  Half-angle planes (c, s).  |V| <= 1: no rescaling.
+//
+// F is never formed: F^T x factorises over the levels.  Summing level k out (k = 0, 1, ...)
+// replaces input bit a_k by output bit b_k with the 2x2 factor RY[a_k ^ b_k][b_{k-1}], whose
+// column b_{k-1} is an output bit already, so one level is a 2x2 rotation of every element
+// pair differing in bit k, selected by bit k-1:
+//     sel 0: (y0, y1) = (c x0 + s x1, s x0 + c x1)     sel 1: (y0, y1) = (-s x0 + c x1, c x0 - s x1)
+// i.e. y0 = p x0 + q x1, y1 = q x0 + p x1 with (p, q) = sel ? (-s, c) : (c, s).  One side costs
+// M passes of D^2 / 2 rotations (2 D^2 M instructions) instead of the D^3 of F^T V.
+// V is flat, e = row * D + col: row bit k sits at bit M + k of e, column bit k at bit k.
+__device__ __forceinline__ void rot_pair(double& x0, double& x1, double c, double s, int sel) {
+  const double p = sel ? -s : c, q = sel ? c : s;
+  const double y0 = fma(p, x0, q * x1), y1 = fma(q, x0, p * x1);
+  x0 = y0;
+  x1 = y1;
+}
+
+__device__ __forceinline__ double ry_delta_mask(int e, int M, double cd, double sd) {
+  const int tb = (e >> (2 * M - 1)) & 1, tc = (e >> (M - 1)) & 1;
+  return tb == tc ? cd : (tb ? sd : -sd);
+}
+
+// Register-resident bond (L = 3, 4: D = 4, 8), one pair per thread, fully unrolled.
 template <int M>
 struct BondG {
-  static constexpr int D = 1 << M;
-  double v[D][D];
+  static constexpr int D = 1 << M, E = D * D;
+  double v[E];
 };
 
-template <int M>
-__device__ __forceinline__ void site_matrix(double (&F)[1 << M][1 << M], double c, double s) {
-  constexpr int D = 1 << M;
+template <int M, int OFF>
+__device__ __forceinline__ void bondg_side(double (&v)[1 << (2 * M)], double c, double s) {
+  constexpr int E = 1 << (2 * M);
 #pragma unroll
-  for (int a = 0; a < D; ++a)
+  for (int k = 0; k < M; ++k)
 #pragma unroll
-    for (int b = 0; b < D; ++b) {
-      double f = 1.0;
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        const int r = ((a >> k) ^ (b >> k)) & 1;            // RY row: a_k ^ b_k
-        const int col = k == 0 ? 0 : ((b >> (k - 1)) & 1);  // RY column: b_{k-1}
-        const double e = col == 0 ? (r ? s : c) : (r ? c : -s);
-        f = k == 0 ? e : f * e;
-      }
-      F[a][b] = f;
+    for (int e = 0; e < E; ++e) {
+      const int pos = OFF + k;
+      if (e & (1 << pos)) continue;
+      rot_pair(v[e], v[e | (1 << pos)], c, s, k == 0 ? 0 : (e >> (pos - 1)) & 1);
     }
 }
 
 template <int M>
 __device__ __forceinline__ void bondg_init(BondG<M>& s) {
 #pragma unroll
-  for (int a = 0; a < BondG<M>::D; ++a)
-#pragma unroll
-    for (int b = 0; b < BondG<M>::D; ++b) s.v[a][b] = (a == 0 && b == 0) ? 1.0 : 0.0;
+  for (int e = 0; e < BondG<M>::E; ++e) s.v[e] = e == 0 ? 1.0 : 0.0;
 }
 
 template <int M>
 __device__ __forceinline__ void bondg_step(BondG<M>& s, double2 vi, double2 vj) {
-  constexpr int D = 1 << M;
-  double Fi[D][D], Fj[D][D], W[D][D];
-  site_matrix<M>(Fi, vi.x, vi.y);
-  site_matrix<M>(Fj, vj.x, vj.y);
-#pragma unroll
-  for (int b = 0; b < D; ++b)  // W = Fi^T V
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double w = Fi[0][b] * s.v[0][a];
-#pragma unroll
-      for (int k = 1; k < D; ++k) w = fma(Fi[k][b], s.v[k][a], w);
-      W[b][a] = w;
-    }
+  bondg_side<M, M>(s.v, vi.x, vi.y);  // F_i^T V  (row index)
+  bondg_side<M, 0>(s.v, vj.x, vj.y);  // (.) F_j  (column index)
   const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
   const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
 #pragma unroll
-  for (int b = 0; b < D; ++b)  // V = (W Fj) o RY(delta)[top bits]
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      double v = W[b][0] * Fj[0][c];
-#pragma unroll
-      for (int k = 1; k < D; ++k) v = fma(W[b][k], Fj[k][c], v);
-      const int tb = (b >> (M - 1)) & 1, tc = (c >> (M - 1)) & 1;
-      const double m = tb == tc ? cd : (tb ? sd : -sd);
-      s.v[b][c] = v * m;
-    }
+  for (int e = 0; e < BondG<M>::E; ++e) s.v[e] *= ry_delta_mask(e, M, cd, sd);
 }
 
 template <int M>
 __device__ __forceinline__ double bondg_amp(const BondG<M>& s) {
   double acc = 0.0;
 #pragma unroll
-  for (int a = 0; a < BondG<M>::D; ++a)
-#pragma unroll
-    for (int b = 0; b < BondG<M>::D; ++b) acc += s.v[a][b];
+  for (int e = 0; e < BondG<M>::E; ++e) acc += s.v[e];
   return acc;
 }
 
@@ -806,6 +798,187 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// L = 5..8 (D = 16..128, state 2 KB..128 KB per pair): the D x D state lives in shared memory
+// and a CTA of 256 threads sweeps PP pairs at once.  Each round applies two levels of one
+// side to element quads held in registers (one shared-memory read and write per element per
+// two levels), one CTA barrier per round: 2 ceil(M/2) rounds per qubit.  RY(delta) is fused
+// into the last column round.  Shared by the tile kernel and the pair-list kernel.
+// ------------------------------------------------------------------------------------------
+constexpr int kDeepThreads = 256;
+template <int M>
+struct Deep {
+  static constexpr int D = 1 << M, E = D * D;
+  static constexpr int PP = M == 4 ? 4 : 1;           // pairs per CTA (M = 4: 64 quads each)
+  static constexpr int kGroups = kTile * kTile / PP;  // pair groups (work items) per tile
+  static constexpr size_t kSmem = size_t(PP) * E * sizeof(double);
+};
+
+__device__ __forceinline__ int insert0(int w, int p) {
+  return ((w >> p) << (p + 1)) | (w & ((1 << p) - 1));
+}
+
+// Levels k0 (and k0 + 1 when nb = 2) of the side whose bits start at `off` (M: rows, 0:
+// columns).  The thread's work items all belong to the slot whose (c, s) it passes.
+template <int M>
+__device__ __forceinline__ void deep_round(double* V, int off, int k0, int nb, double c, double s,
+                                           bool mask, double cd, double sd) {
+  constexpr int E = Deep<M>::E;
+  const int per_slot = E >> nb, total = Deep<M>::PP * per_slot;
+  const int p0 = off + k0;
+  for (int w = threadIdx.x; w < total; w += kDeepThreads) {
+    double* v = V + (w / per_slot) * E;
+    const int lw = w % per_slot;
+    if (nb == 2) {
+      const int base = insert0(insert0(lw, p0), p0 + 1);
+      const int e01 = base | (1 << p0), e10 = base | (2 << p0), e11 = e01 | e10;
+      double x00 = v[base], x01 = v[e01], x10 = v[e10], x11 = v[e11];
+      const int sel = k0 == 0 ? 0 : (base >> (p0 - 1)) & 1;
+      rot_pair(x00, x01, c, s, sel);  // level k0: pairs differing in bit p0
+      rot_pair(x10, x11, c, s, sel);
+      rot_pair(x00, x10, c, s, 0);    // level k0 + 1, selected by bit p0 of the element
+      rot_pair(x01, x11, c, s, 1);
+      if (mask) {
+        x00 *= ry_delta_mask(base, M, cd, sd);
+        x01 *= ry_delta_mask(e01, M, cd, sd);
+        x10 *= ry_delta_mask(e10, M, cd, sd);
+        x11 *= ry_delta_mask(e11, M, cd, sd);
+      }
+      v[base] = x00;
+      v[e01] = x01;
+      v[e10] = x10;
+      v[e11] = x11;
+    } else {
+      const int e0 = insert0(lw, p0), e1 = e0 | (1 << p0);
+      double x0 = v[e0], x1 = v[e1];
+      rot_pair(x0, x1, c, s, k0 == 0 ? 0 : (e0 >> (p0 - 1)) & 1);
+      if (mask) {
+        x0 *= ry_delta_mask(e0, M, cd, sd);
+        x1 *= ry_delta_mask(e1, M, cd, sd);
+      }
+      v[e0] = x0;
+      v[e1] = x1;
+    }
+  }
+}
+
+// Sweeps the PP pairs whose plane columns (qubit 0) are pi / pj for this thread's slot;
+// leaves amp of slot s in red[s * (kDeepThreads / PP)].  Starts and ends with a barrier.
+template <int M>
+__device__ __forceinline__ void deep_sweep(double* V, double* red, const double2* pi,
+                                           const double2* pj, int q_begin, int q_end) {
+  constexpr int E = Deep<M>::E, PP = Deep<M>::PP, TPS = kDeepThreads / PP;
+  for (int e = threadIdx.x; e < PP * E; e += kDeepThreads) V[e] = (e % E) == 0 ? 1.0 : 0.0;
+  __syncthreads();
+  for (int q = q_begin; q < q_end; ++q) {
+    const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
+    const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
+    const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
+    for (int k0 = 0; k0 < M; k0 += 2) {
+      deep_round<M>(V, M, k0, M - k0 >= 2 ? 2 : 1, vi.x, vi.y, false, cd, sd);
+      __syncthreads();
+    }
+    for (int k0 = 0; k0 < M; k0 += 2) {
+      deep_round<M>(V, 0, k0, M - k0 >= 2 ? 2 : 1, vj.x, vj.y, k0 + 2 >= M, cd, sd);
+      __syncthreads();
+    }
+  }
+  // amp = sum(V) per slot: TPS threads per slot, fixed order
+  const int slot = threadIdx.x / TPS, lt = threadIdx.x % TPS;
+  double acc = 0.0;
+  for (int e = lt; e < E; e += TPS) acc += V[slot * E + e];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (lt == 0) {
+    double t = 0.0;
+    for (int k = 0; k < TPS; ++k) t += red[threadIdx.x + k];
+    red[threadIdx.x] = t;  // only this thread reads/writes its group's first entry now
+  }
+  __syncthreads();
+}
+
+template <int M, int MODE, int OUT>
+__global__ void __launch_bounds__(kDeepThreads) sweep_deep_kernel(const SweepArgs a) {
+  extern __shared__ double V[];
+  __shared__ double red[kDeepThreads];
+  constexpr int PP = Deep<M>::PP, G = Deep<M>::kGroups, TPS = kDeepThreads / PP;
+  const int my_slot = threadIdx.x / TPS;
+  const int64_t items = a.n_tiles * G;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t g = a.tile_begin + it / G;
+    const int grp = int(it % G);
+    int64_t bi, bj;
+    if (MODE == kModeGram) {
+      decode_upper(g, a.nb_rows, bi, bj);
+    } else {
+      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+    }
+    // does any pair of the group need computing?  (uniform: every thread evaluates all)
+    bool any = false;
+#pragma unroll
+    for (int sl = 0; sl < PP; ++sl) {
+      const int pl = grp * PP + sl;
+      const int64_t i = bi * kTile + pl / kTile - a.pad_rows, j = bj * kTile + pl % kTile - a.pad_cols;
+      any |= MODE == kModeGram ? (i >= 0 && i < j && j < a.n_rows)
+                               : (i >= 0 && j >= 0 && i < a.n_rows && j < a.n_cols);
+    }
+    const int pl = grp * PP + my_slot, il = pl / kTile, jl = pl % kTile;
+    if (any) {
+      deep_sweep<M>(V, red, a.rows + bi * int64_t(a.n_pad) * kTile + il,
+                    a.cols + bj * int64_t(a.n_pad) * kTile + jl, a.front, a.n_pad);
+    }
+    if (threadIdx.x % TPS == 0) {
+      const int64_t i = bi * kTile + il - a.pad_rows, j = bj * kTile + jl - a.pad_cols;
+      const bool need = MODE == kModeGram ? (i >= 0 && i < j && j < a.n_rows)
+                                          : (i >= 0 && j >= 0 && i < a.n_rows && j < a.n_cols);
+      const double v = need ? kernel_value(red[threadIdx.x], a.convention) : 0.0;
+      if (OUT == QK_OUT_PACKED) {
+        a.out[(g - a.tile_begin) * int64_t(kTile * kTile) + pl] = v;
+      } else if (MODE == kModeGram) {
+        if (need) {
+          a.out[i * a.ld_out + j] = v;
+          a.out[j * a.ld_out + i] = v;
+        } else if (i == j && i >= 0 && i < a.n_rows) {
+          a.out[i * a.ld_out + i] = 1.0;
+        }
+      } else if (need) {
+        a.out[i * a.ld_out + j] = v;
+      }
+    }
+    __syncthreads();  // red and V are reused by the next item
+    if (a.progress != nullptr) {
+      if (threadIdx.x % TPS == 0) QK_PROGRESS_FENCE();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(a.progress + bi, 1u);  // G per tile
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kDeepThreads) pairs_deep_kernel(
+    const double2* __restrict__ A, int64_t n_a, const double2* __restrict__ B, int64_t n_b,
+    const int64_t* __restrict__ pairs, int64_t n_pairs, double* __restrict__ amp, int n_pad,
+    int front) {
+  extern __shared__ double V[];
+  __shared__ double red[kDeepThreads];
+  constexpr int PP = Deep<M>::PP, TPS = kDeepThreads / PP;
+  const int my_slot = threadIdx.x / TPS;
+  const int64_t k = int64_t(blockIdx.x) * PP + my_slot;
+  int64_t p = 0, q = 0;
+  bool ok = false;
+  if (k < n_pairs) {
+    p = pairs[2 * k];
+    q = pairs[2 * k + 1];
+    ok = p >= 0 && p < n_a && q >= 0 && q < n_b;
+  }
+  if (!ok) p = q = 0;  // sweep a valid column; the result is discarded
+  const int64_t sp = p + sample_pad(n_a), sq = q + sample_pad(n_b);  // plane slots
+  deep_sweep<M>(V, red, A + (sp / kTile) * int64_t(n_pad) * kTile + (sp % kTile),
+                B + (sq / kTile) * int64_t(n_pad) * kTile + (sq % kTile), front, n_pad);
+  if (threadIdx.x % TPS == 0 && k < n_pairs)
+    amp[k] = ok ? red[threadIdx.x] : __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// ------------------------------------------------------------------------------------------
 // Pair-list kernel: one pair per thread, planes read straight from global/L2.
 // ------------------------------------------------------------------------------------------
 template <int LAYERS>
@@ -971,6 +1144,48 @@ static qk_status launch_general(const SweepArgs& a, cudaStream_t st) {
   return cuda_status(cudaGetLastError(), "general sweep launch");
 }
 
+template <int M, int MODE, int OUT>
+static qk_status launch_deep(const SweepArgs& a, cudaStream_t st) {
+  auto kern = sweep_deep_kernel<M, MODE, OUT>;
+  constexpr size_t smem = Deep<M>::kSmem;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return cuda_status(e, "deep sweep smem attribute");
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDeepThreads, smem);
+  if (e != cudaSuccess) return cuda_status(e, "deep sweep occupancy");
+  const int sms = sm_count();
+  if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
+  int64_t grid = int64_t(sms) * (per_sm < 1 ? 1 : per_sm);
+  const int64_t items = a.n_tiles * Deep<M>::kGroups;
+  if (grid > items) grid = items;
+  kern<<<unsigned(grid), kDeepThreads, smem, st>>>(a);
+  return cuda_status(cudaGetLastError(), "deep sweep launch");
+}
+
+template <int M>
+static qk_status launch_deep_t(const SweepArgs& a, int mode, bool packed, cudaStream_t st) {
+  if (mode == kModeGram)
+    return packed ? launch_deep<M, kModeGram, QK_OUT_PACKED>(a, st)
+                  : launch_deep<M, kModeGram, QK_OUT_DENSE>(a, st);
+  return packed ? launch_deep<M, kModeCross, QK_OUT_PACKED>(a, st)
+                : launch_deep<M, kModeCross, QK_OUT_DENSE>(a, st);
+}
+
+template <int M>
+static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, const void* d_b,
+                                   int64_t n_b, const int64_t* d_pairs, int64_t n_pairs,
+                                   double* d_amp, cudaStream_t st) {
+  auto kern = pairs_deep_kernel<M>;
+  constexpr size_t smem = Deep<M>::kSmem;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return cuda_status(e, "deep pairs smem attribute");
+  const int64_t grid = (n_pairs + Deep<M>::PP - 1) / Deep<M>::PP;
+  kern<<<unsigned(grid), kDeepThreads, smem, st>>>(
+      static_cast<const double2*>(d_a), n_a, static_cast<const double2*>(d_b), n_b, d_pairs,
+      n_pairs, d_amp, p.width_padded, p.front_pad);
+  return cuda_status(cudaGetLastError(), "deep pairs launch");
+}
+
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
@@ -1010,6 +1225,13 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
                     : launch_sweep_t<1, kModeGram, QK_OUT_DENSE>(a, st);
     return packed ? launch_sweep_t<1, kModeCross, QK_OUT_PACKED>(a, st)
                   : launch_sweep_t<1, kModeCross, QK_OUT_DENSE>(a, st);
+  }
+  switch (p.layers) {
+    case 5: return launch_deep_t<4>(a, mode, packed, st);
+    case 6: return launch_deep_t<5>(a, mode, packed, st);
+    case 7: return launch_deep_t<6>(a, mode, packed, st);
+    case 8: return launch_deep_t<7>(a, mode, packed, st);
+    default: break;
   }
   if (p.layers == 4) {
     if (mode == kModeGram)
@@ -1095,6 +1317,13 @@ qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* 
   const unsigned grid = unsigned((n_pairs + 127) / 128);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nchunks = p.width_padded / kChunk;
+  switch (p.layers) {
+    case 5: return launch_pairs_deep<4>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
+    case 6: return launch_pairs_deep<5>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
+    case 7: return launch_pairs_deep<6>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
+    case 8: return launch_pairs_deep<7>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
+    default: break;
+  }
   if (p.layers == 2)
     pairs_kernel<2><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,

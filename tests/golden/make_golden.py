@@ -6,6 +6,7 @@ not exist on the GPU box):
     python tests/golden/make_golden.py        # the contract_batch cases + known answers
     python tests/golden/make_golden.py sv     # the state-vector cases (sv_*.npz)
     python tests/golden/make_golden.py l4     # layers = 4 cases
+    python tests/golden/make_golden.py deep   # layers 5 to 8 cases
 
 Each case stores the angles, the pair list and the reference amplitudes returned by
 ``contract_batch(template, pairs, plan_contraction(template), workers)``
@@ -147,7 +148,22 @@ def l4_cases():
     sampled_case("pairs_n24_L4", rng, 10, 24, 4, 0.1, 12)
 
 
+def deep_cases():
+    """layers 5 to 8 (bond 4^(L-1) transfer; the GPU's shared-memory deep sweep): the
+    reference's contract_batch on small widths (its cost grows ~4^L per qubit)."""
+    rng = np.random.default_rng(240502630 + 5)
+    gram_case("gram_n5_L5", rng, 8, 5, 5, 0.4)
+    sampled_case("pairs_n24_L5", rng, 10, 24, 5, 0.1, 8)
+    cross_case("cross_n7_L6", rng, 3, 4, 7, 6, 0.3)
+    sampled_case("pairs_n10_L6", rng, 8, 10, 6, 0.2, 6)
+    sampled_case("pairs_n8_L7", rng, 6, 8, 7, 0.3, 5)
+    sampled_case("pairs_n6_L8", rng, 5, 6, 8, 0.4, 4)
+
+
 def main():
+    if sys.argv[1:] == ["deep"]:
+        deep_cases()
+        return
     if sys.argv[1:] == ["sv"]:
         sv_cases()
         return

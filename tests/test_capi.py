@@ -33,7 +33,7 @@ def test_library_is_built_for_sm100a():
     (0, 2, 0, ValueError, "width must be >= 1"),
     (4, 0, 0, ValueError, "layers must be >= 1"),
     (4, 2, 7, ValueError, "unknown kernel convention"),
-    (4, 5, 0, CapacityError, "bond-256"),
+    (4, 9, 0, CapacityError, "bond-65536"),
 ])
 def test_plan_validation_through_the_abi(width, layers, conv, exc, msg):
     lib = _native.lib()
@@ -58,8 +58,12 @@ def test_plan_geometry_and_costs():
     assert q.info["width_padded"] == 32  # 15 identity qubits in front
     assert SweepPlan(5, 1).info["bond"] == 1
     assert SweepPlan(5, 3).info["bond"] == 16
-    assert SweepPlan(5, 4).info["bond"] == 64
-    assert SweepPlan(5, 3).info["dp_instr_per_entry"] == 180 * 5 + 15  # D = 4 transfer
+    for L in (3, 4, 5, 6, 7, 8):  # factored level passes: (4 M E + E + 4) n + E instructions
+        M, E = L - 1, 4 ** (L - 1)
+        info = SweepPlan(5, L).info
+        assert info["bond"] == E
+        assert info["dp_instr_per_entry"] == (4 * M * E + E + 4) * 5 + E
+    assert SweepPlan(5, 3).info["dp_instr_per_entry"] == 148 * 5 + 16  # D = 4 transfer
 
 
 def test_null_and_range_arguments_are_rejected():
