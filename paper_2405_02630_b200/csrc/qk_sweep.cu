@@ -798,100 +798,124 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
-// L = 5..8 (D = 16..128, state 2 KB..128 KB per pair): the D x D state lives in shared memory
-// and a CTA of 256 threads sweeps PP pairs at once.  Each round applies two levels of one
-// side to element quads held in registers (one shared-memory read and write per element per
-// two levels), one CTA barrier per round: 2 ceil(M/2) rounds per qubit.  RY(delta) is fused
-// into the last column round.  Shared by the tile kernel and the pair-list kernel.
+// L = 5..8 (D = 16..128, state 2 KB..128 KB per pair): the D x D state of PP pairs lives in
+// shared memory (rows padded to D + 1 doubles: conflict-free row and column walks) and a CTA
+// of 256 threads sweeps them.  Per qubit two register rounds: each thread loads one column
+// (F_i side: all M row-level passes in registers) or one row (F_j side + the RY(delta) mask),
+// so every element crosses shared memory once per side; a CTA barrier after each round.  At
+// L = 8 (D = 128) a thread holds half a column / row (64 values) and the top level is one
+// extra pair round.  Shared by the tile kernel and the pair-list kernel (bit-identical).
 // ------------------------------------------------------------------------------------------
 constexpr int kDeepThreads = 256;
 template <int M>
 struct Deep {
-  static constexpr int D = 1 << M, E = D * D;
-  static constexpr int PP = M == 4 ? 4 : 1;           // pairs per CTA (M = 4: 64 quads each)
+  static constexpr int D = 1 << M, E = D * D, RS = D + 1;  // padded row stride (doubles)
+  static constexpr int G = M < 6 ? M : 6;    // levels per register round (2^G values/thread)
+  static constexpr int H = M - G;            // remaining levels: pair rounds (M = 7: one)
+  static constexpr int IPP = D << H;         // threads per pair
+  static constexpr int PP = kDeepThreads / IPP;       // pairs per CTA: 16, 8, 4, 1
   static constexpr int kGroups = kTile * kTile / PP;  // pair groups (work items) per tile
-  static constexpr size_t kSmem = size_t(PP) * E * sizeof(double);
+  static constexpr int kSlot = D * RS;                // doubles per pair
+  static constexpr size_t kSmem = size_t(PP) * kSlot * sizeof(double);
 };
+
+static_assert(progress_unit(5) == Deep<4>::kGroups && progress_unit(6) == Deep<5>::kGroups &&
+                  progress_unit(7) == Deep<6>::kGroups && progress_unit(8) == Deep<7>::kGroups,
+              "host progress unit = deep pair groups per tile");
 
 __device__ __forceinline__ int insert0(int w, int p) {
   return ((w >> p) << (p + 1)) | (w & ((1 << p) - 1));
 }
 
-// Levels k0 (and k0 + 1 when nb = 2) of the side whose bits start at `off` (M: rows, 0:
-// columns).  The thread's work items all belong to the slot whose (c, s) it passes.
-template <int M>
-__device__ __forceinline__ void deep_round(double* V, int off, int k0, int nb, double c, double s,
-                                           bool mask, double cd, double sd) {
-  constexpr int E = Deep<M>::E;
-  const int per_slot = E >> nb, total = Deep<M>::PP * per_slot;
-  const int p0 = off + k0;
-  for (int w = threadIdx.x; w < total; w += kDeepThreads) {
-    double* v = V + (w / per_slot) * E;
-    const int lw = w % per_slot;
-    if (nb == 2) {
-      const int base = insert0(insert0(lw, p0), p0 + 1);
-      const int e01 = base | (1 << p0), e10 = base | (2 << p0), e11 = e01 | e10;
-      double x00 = v[base], x01 = v[e01], x10 = v[e10], x11 = v[e11];
-      const int sel = k0 == 0 ? 0 : (base >> (p0 - 1)) & 1;
-      rot_pair(x00, x01, c, s, sel);  // level k0: pairs differing in bit p0
-      rot_pair(x10, x11, c, s, sel);
-      rot_pair(x00, x10, c, s, 0);    // level k0 + 1, selected by bit p0 of the element
-      rot_pair(x01, x11, c, s, 1);
-      if (mask) {
-        x00 *= ry_delta_mask(base, M, cd, sd);
-        x01 *= ry_delta_mask(e01, M, cd, sd);
-        x10 *= ry_delta_mask(e10, M, cd, sd);
-        x11 *= ry_delta_mask(e11, M, cd, sd);
-      }
-      v[base] = x00;
-      v[e01] = x01;
-      v[e10] = x10;
-      v[e11] = x11;
-    } else {
-      const int e0 = insert0(lw, p0), e1 = e0 | (1 << p0);
-      double x0 = v[e0], x1 = v[e1];
-      rot_pair(x0, x1, c, s, k0 == 0 ? 0 : (e0 >> (p0 - 1)) & 1);
-      if (mask) {
-        x0 *= ry_delta_mask(e0, M, cd, sd);
-        x1 *= ry_delta_mask(e1, M, cd, sd);
-      }
-      v[e0] = x0;
-      v[e1] = x1;
+// One side of one qubit for this thread's column (COLS = false: F_i^T on the row index) or
+// row (COLS = true: F_j on the column index, then the RY(delta) mask when H = 0).
+template <int M, bool COLS>
+__device__ __forceinline__ void deep_reg_round(double* V, double c, double s, double cd,
+                                               double sd) {
+  using Dp = Deep<M>;
+  constexpr int D = Dp::D, RS = Dp::RS, G = Dp::G, N = 1 << G;
+  const int w = threadIdx.x % Dp::IPP;
+  const int lo = w % D, hi = w / D;  // lo: the fixed column (row side) or row (column side)
+  double* base = V + (threadIdx.x / Dp::IPP) * Dp::kSlot + (COLS ? lo * RS : lo);
+  constexpr int step = COLS ? 1 : RS;
+  double x[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) x[k] = base[((hi << G) | k) * step];
+#pragma unroll
+  for (int k = 0; k < G; ++k)
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      if (e & (1 << k)) continue;
+      rot_pair(x[e], x[e | (1 << k)], c, s, k == 0 ? 0 : (e >> (k - 1)) & 1);
     }
+  if (COLS && Dp::H == 0) {  // top row bit = bit M-1 of lo, top column bit = bit M-1 of k
+    const bool tb = (lo >> (M - 1)) & 1;
+    const double m0 = tb ? sd : cd, m1 = tb ? cd : -sd;
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] *= ((k >> (M - 1)) & 1) ? m1 : m0;
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) base[((hi << G) | k) * step] = x[k];
+}
+
+// The top level (bit G of the side) as element-pair rotations, L = 8 only.
+template <int M, bool COLS>
+__device__ __forceinline__ void deep_pair_round(double* V, double c, double s, double cd,
+                                                double sd) {
+  using Dp = Deep<M>;
+  constexpr int D = Dp::D, RS = Dp::RS, p0 = (COLS ? 0 : M) + Dp::G;
+  for (int w = threadIdx.x; w < Dp::PP * (Dp::E / 2); w += kDeepThreads) {
+    double* v = V + (w / (Dp::E / 2)) * Dp::kSlot;
+    const int e0 = insert0(w % (Dp::E / 2), p0), e1 = e0 | (1 << p0);
+    const int a0 = (e0 >> M) * RS + (e0 & (D - 1)), a1 = (e1 >> M) * RS + (e1 & (D - 1));
+    double x0 = v[a0], x1 = v[a1];
+    rot_pair(x0, x1, c, s, (e0 >> (p0 - 1)) & 1);
+    if (COLS) {
+      x0 *= ry_delta_mask(e0, M, cd, sd);
+      x1 *= ry_delta_mask(e1, M, cd, sd);
+    }
+    v[a0] = x0;
+    v[a1] = x1;
   }
 }
 
 // Sweeps the PP pairs whose plane columns (qubit 0) are pi / pj for this thread's slot;
-// leaves amp of slot s in red[s * (kDeepThreads / PP)].  Starts and ends with a barrier.
+// leaves amp of slot s in red[s * IPP].  Starts and ends with a barrier.
 template <int M>
 __device__ __forceinline__ void deep_sweep(double* V, double* red, const double2* pi,
                                            const double2* pj, int q_begin, int q_end) {
-  constexpr int E = Deep<M>::E, PP = Deep<M>::PP, TPS = kDeepThreads / PP;
-  for (int e = threadIdx.x; e < PP * E; e += kDeepThreads) V[e] = (e % E) == 0 ? 1.0 : 0.0;
+  using Dp = Deep<M>;
+  for (int e = threadIdx.x; e < Dp::PP * Dp::kSlot; e += kDeepThreads)
+    V[e] = (e % Dp::kSlot) == 0 ? 1.0 : 0.0;
   __syncthreads();
   for (int q = q_begin; q < q_end; ++q) {
     const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
     const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
     const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
-    for (int k0 = 0; k0 < M; k0 += 2) {
-      deep_round<M>(V, M, k0, M - k0 >= 2 ? 2 : 1, vi.x, vi.y, false, cd, sd);
+    deep_reg_round<M, false>(V, vi.x, vi.y, cd, sd);
+    __syncthreads();
+    if constexpr (Dp::H > 0) {
+      deep_pair_round<M, false>(V, vi.x, vi.y, cd, sd);
       __syncthreads();
     }
-    for (int k0 = 0; k0 < M; k0 += 2) {
-      deep_round<M>(V, 0, k0, M - k0 >= 2 ? 2 : 1, vj.x, vj.y, k0 + 2 >= M, cd, sd);
+    deep_reg_round<M, true>(V, vj.x, vj.y, cd, sd);
+    __syncthreads();
+    if constexpr (Dp::H > 0) {
+      deep_pair_round<M, true>(V, vj.x, vj.y, cd, sd);
       __syncthreads();
     }
   }
-  // amp = sum(V) per slot: TPS threads per slot, fixed order
-  const int slot = threadIdx.x / TPS, lt = threadIdx.x % TPS;
+  // amp = sum(V) per slot (padding entries are zero): IPP threads per slot, fixed order
+  const int w = threadIdx.x % Dp::IPP;
+  const double* v = V + (threadIdx.x / Dp::IPP) * Dp::kSlot;
   double acc = 0.0;
-  for (int e = lt; e < E; e += TPS) acc += V[slot * E + e];
+  for (int e = w; e < Dp::kSlot; e += Dp::IPP) acc += v[e];
   red[threadIdx.x] = acc;
   __syncthreads();
-  if (lt == 0) {
+  if (w == 0) {
     double t = 0.0;
-    for (int k = 0; k < TPS; ++k) t += red[threadIdx.x + k];
-    red[threadIdx.x] = t;  // only this thread reads/writes its group's first entry now
+    for (int k = 0; k < Dp::IPP; ++k) t += red[threadIdx.x + k];
+    red[threadIdx.x] = t;  // only this thread touches its group's first entry now
   }
   __syncthreads();
 }
@@ -900,7 +924,7 @@ template <int M, int MODE, int OUT>
 __global__ void __launch_bounds__(kDeepThreads) sweep_deep_kernel(const SweepArgs a) {
   extern __shared__ double V[];
   __shared__ double red[kDeepThreads];
-  constexpr int PP = Deep<M>::PP, G = Deep<M>::kGroups, TPS = kDeepThreads / PP;
+  constexpr int PP = Deep<M>::PP, G = Deep<M>::kGroups, TPS = Deep<M>::IPP;
   const int my_slot = threadIdx.x / TPS;
   const int64_t items = a.n_tiles * G;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -960,7 +984,7 @@ __global__ void __launch_bounds__(kDeepThreads) pairs_deep_kernel(
     int front) {
   extern __shared__ double V[];
   __shared__ double red[kDeepThreads];
-  constexpr int PP = Deep<M>::PP, TPS = kDeepThreads / PP;
+  constexpr int PP = Deep<M>::PP, TPS = Deep<M>::IPP;
   const int my_slot = threadIdx.x / TPS;
   const int64_t k = int64_t(blockIdx.x) * PP + my_slot;
   int64_t p = 0, q = 0;
