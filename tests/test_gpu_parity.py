@@ -316,3 +316,27 @@ def test_config3_fashion_784_sampled_and_ovr_accuracy():
     clf = OneVsRestClassifier(SVC(kernel="precomputed", C=1.0)).fit(K.entries, ytr)
     acc = float((clf.predict(Kx.entries) == yte).mean())
     assert acc > 0.5  # 10-class synthetic Fashion: far above the 0.1 chance level
+
+
+@pytest.mark.parametrize("n", [1600, 2100])
+def test_wide_chains_cross_rescale_points(n, rng):
+    """n > 1024: the L = 2 sweep rescales its state by 2^-512 every 512 qubits (3-4 times
+    here) and pads the front of the chain; tightly clustered samples keep K ~ 1e-2..1."""
+    X = rng.uniform(0, np.pi, n) + rng.normal(0, 0.02, (70, n))
+    T = X[:5] + rng.normal(0, 0.01, (5, n))
+    cfg = FeatureMapConfig(n)
+    K = compute_kernel_matrix(X, cfg).entries
+    Kx = compute_cross_kernel(T, X, cfg).entries
+    Kr, Kxr = oracle.kernel_matrix(X, 2), oracle.cross_kernel(T, X, 2)
+    assert np.abs(K - Kr).max() <= K_ABS and np.abs(Kx - Kxr).max() <= K_ABS
+    assert np.all(np.abs(np.sqrt(K) - np.sqrt(Kr)) <= AMP_REL * np.sqrt(Kr) + 1e-300)
+
+
+def test_large_and_negative_angles(rng):
+    """Any finite angle is valid (the reference only checks finiteness, circuit.py:112-118):
+    large magnitudes and negative values against the oracle for L = 1, 2, 3, 5."""
+    X = rng.normal(0, 1, (40, 9)) * np.array([1, 10, 100, 1e3, 1e4, 1e5, -1e6, 3e7, -1e8])
+    X[5] = X[4] + 1e-3
+    for L in (1, 2, 3, 5):
+        K = compute_kernel_matrix(X, FeatureMapConfig(9, layers=L)).entries
+        assert np.abs(K - oracle.kernel_matrix(X, L)).max() <= K_ABS, L

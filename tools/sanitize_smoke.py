@@ -1,5 +1,5 @@
 """Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck /
-synccheck): gate build, joint sweep (L = 1, 2, 3), dense + packed + unpack, pair kernel,
+synccheck): gate build, joint sweep (L = 1..8), dense + packed + unpack, pair kernel,
 host pipelines (pinned and pageable)."""
 import sys
 from pathlib import Path
@@ -13,20 +13,21 @@ from paper_2405_02630_b200 import (FeatureMapConfig, SweepPlan,  # noqa: E402
 from paper_2405_02630_b200 import device as dev  # noqa: E402
 
 rng = np.random.default_rng(0)
-for L, n in ((2, 40), (1, 20), (3, 6)):
-    Xtr = rng.uniform(0, 1, (150, n))
-    Xte = rng.uniform(0, 1, (70, n))
+for L, n in ((2, 40), (1, 20), (3, 6), (4, 5), (5, 4), (6, 3), (7, 3), (8, 2)):
+    Ntr, Nte = (150, 70) if L <= 4 else (40, 9) if L <= 6 else (12, 3)
+    Xtr = rng.uniform(0, 1, (Ntr, n))
+    Xte = rng.uniform(0, 1, (Nte, n))
     cfg = FeatureMapConfig(n, layers=L)
     K, Kx = compute_kernel_matrices(Xtr, Xte, cfg)
     plan = SweepPlan(n, L)
     pt = dev.gate_build(plan, torch.as_tensor(Xtr, device="cuda"))
     ps = dev.gate_build(plan, torch.as_tensor(Xte, device="cuda"))
-    nt = plan.gram_tile_count(150)
+    nt = plan.gram_tile_count(Ntr)
     packed = dev.gram(pt, packed=True)
-    Kd = torch.zeros((150, 150), dtype=torch.float64, device="cuda")
-    dev.unpack_gram(plan, packed, 150, 0, nt, Kd)
+    Kd = torch.zeros((Ntr, Ntr), dtype=torch.float64, device="cuda")
+    dev.unpack_gram(plan, packed, Ntr, 0, nt, Kd)
     Kxd = dev.cross(ps, pt)
-    pairs = torch.as_tensor(np.array([[0, 1], [5, 149], [149, 0]]), device="cuda")
+    pairs = torch.as_tensor(np.array([[0, 1], [5, Ntr - 1], [Ntr - 1, 0]]), device="cuda")
     amp = dev.pair_amplitudes(pt, pt, pairs)
     torch.cuda.synchronize()
     assert np.array_equal(Kd.cpu().numpy(), K.entries)
