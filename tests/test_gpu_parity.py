@@ -340,3 +340,19 @@ def test_large_and_negative_angles(rng):
     for L in (1, 2, 3, 5):
         K = compute_kernel_matrix(X, FeatureMapConfig(9, layers=L)).entries
         assert np.abs(K - oracle.kernel_matrix(X, L)).max() <= K_ABS, L
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 5])
+def test_spec_invariants_range_and_psd(L, rng):
+    """SPEC kernel_pipeline invariants: entries in [0, 1 + 1e-9]; the probability-convention
+    Gram is positive semidefinite (smallest eigenvalue >= -1e-8, K_ij = Tr(rho_i rho_j));
+    a test point identical to a train point gives 1 at that column."""
+    n = 12 if L <= 3 else 6
+    X = rng.uniform(0, np.pi, n) + rng.normal(0, 0.4, (120, n))
+    cfg = FeatureMapConfig(n, layers=L)
+    K = compute_kernel_matrix(X, cfg).entries
+    assert K.min() >= 0.0 and K.max() <= 1.0 + 1e-9
+    assert np.linalg.eigvalsh(K).min() >= -1e-8
+    Kx = compute_cross_kernel(X[[7, 30]], X, cfg).entries
+    assert Kx.min() >= 0.0 and Kx.max() <= 1.0 + 1e-9
+    assert abs(Kx[0, 7] - 1.0) <= 1e-9 and abs(Kx[1, 30] - 1.0) <= 1e-9

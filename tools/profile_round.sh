@@ -11,6 +11,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:swee
   -o gpurun_out/prof_sweep_$TAG python tools/profile_sweep.py > gpurun_out/ncu_sweep_$TAG.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:gate_build -c 1 \
   -o gpurun_out/prof_gate_$TAG python tools/profile_sweep.py > gpurun_out/ncu_gate_$TAG.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sweep_deep -c 1 \
+  -o gpurun_out/prof_deep_$TAG python tools/layers_bench.py 5 > gpurun_out/ncu_deep_$TAG.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sweep_general -c 1 \
+  -o gpurun_out/prof_general_$TAG python tools/layers_bench.py 3 > gpurun_out/ncu_general_$TAG.log 2>&1
 ./tools/rfbench > gpurun_out/rfbench_$TAG.txt 2>&1
 ./tools/dmma_bench > gpurun_out/dmma_$TAG.txt 2>&1
 timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
