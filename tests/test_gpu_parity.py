@@ -356,3 +356,37 @@ def test_spec_invariants_range_and_psd(L, rng):
     Kx = compute_cross_kernel(X[[7, 30]], X, cfg).entries
     assert Kx.min() >= 0.0 and Kx.max() <= 1.0 + 1e-9
     assert abs(Kx[0, 7] - 1.0) <= 1e-9 and abs(Kx[1, 30] - 1.0) <= 1e-9
+
+
+def test_large_sample_count_device_gram(rng):
+    """N = 70,000 samples (a 39 GB dense Gram, 2.45e9 entries, 1.2e6 tiles; int64 offsets
+    beyond 2^31 everywhere): sampled entries against the oracle, mirror and unit diagonal."""
+    N, n = 70000, 8
+    X = torch.as_tensor(rng.uniform(0, np.pi, n) + rng.normal(0, 0.3, (N, n)), device="cuda")
+    plan = SweepPlan(n, 2)
+    K = dev.gram(dev.gate_build(plan, X))
+    torch.cuda.synchronize()
+    Xh = X.cpu().numpy()
+    idx = np.concatenate([[0, 1, N - 2, N - 1], rng.integers(0, N, 60)])
+    i, j = np.meshgrid(idx, idx, indexing="ij")
+    got = K[torch.as_tensor(i, device="cuda"), torch.as_tensor(j, device="cuda")].cpu().numpy()
+    sel = np.unique(idx)
+    ref = oracle.kernel_matrix(Xh[sel], 2)
+    pos = {v: k for k, v in enumerate(sel)}
+    want = np.array([[ref[pos[a], pos[b]] for b in idx] for a in idx])
+    assert np.abs(got - want).max() <= K_ABS
+    assert np.array_equal(got, got.T)
+    del K
+    torch.cuda.empty_cache()
+
+
+def test_empty_cross_blocks_and_joint_pass():
+    from paper_2405_02630_b200 import compute_kernel_matrices
+
+    cfg = FeatureMapConfig(5)
+    X = np.random.default_rng(3).uniform(0, 1, (7, 5))
+    assert compute_cross_kernel(np.zeros((0, 5)), X, cfg).entries.shape == (0, 7)
+    assert compute_cross_kernel(X, np.zeros((0, 5)), cfg).entries.shape == (7, 0)
+    K, Kx = compute_kernel_matrices(X, np.zeros((0, 5)), cfg)
+    assert K.entries.shape == (7, 7) and Kx.entries.shape == (0, 7)
+    assert np.abs(K.entries - oracle.kernel_matrix(X, 2)).max() <= K_ABS
