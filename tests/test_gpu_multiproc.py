@@ -28,7 +28,7 @@ def _data():
             centre + rng.normal(0, 0.1, (N_TEST, WIDTH)))
 
 
-def worker(rank, world, port, placement, q):
+def worker(rank, world, port, placement, layers, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         torch.cuda.set_device(0)
@@ -38,13 +38,13 @@ def worker(rank, world, port, placement, q):
         from paper_2405_02630_b200.distributed import KernelJob
 
         Xtr, Xte = _data()
-        plan = SweepPlan(WIDTH, 2)
+        plan = SweepPlan(WIDTH, layers)
         job = KernelJob(plan, N_TRAIN, N_TEST, placement=placement)
         for _ in range(2):  # the second run reuses the shared matrices / buffers
             K, Kx = job.run(torch.as_tensor(Xtr, device="cuda"),
                             torch.as_tensor(Xte, device="cuda"))
         if rank == 0:
-            cfg = FeatureMapConfig(WIDTH)
+            cfg = FeatureMapConfig(WIDTH, layers=layers)
             ok = (np.array_equal(K.cpu().numpy(), compute_kernel_matrix(Xtr, cfg).entries),
                   np.array_equal(Kx.cpu().numpy(), compute_cross_kernel(Xte, Xtr, cfg).entries))
             q.put(ok)
@@ -63,12 +63,15 @@ def _free_port():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("placement", ["p2p", "gather"])
-def test_two_rank_job_matches_single_process(placement):
+@pytest.mark.parametrize("placement,world,layers", [("p2p", 2, 2), ("gather", 2, 2),
+                                                    ("p2p", 3, 2), ("p2p", 3, 5),
+                                                    ("gather", 3, 3)])
+def test_multi_rank_job_matches_single_process(placement, world, layers):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, placement, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, world, port, placement, layers, q))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=500)
