@@ -36,8 +36,11 @@ struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
-  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // angles, planes, K, progress
-  size_t cap[4] = {0, 0, 0, 0};
+  cudaStream_t h2d_stream = nullptr;  // chunked H2D feeding the in-kernel plane build
+  // angles, planes, K, progress, plane-block build states, chunk arrival marks
+  void* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t cap[6] = {0, 0, 0, 0, 0, 0};
+  uint32_t epoch = 0;  // arrival marks hold the epoch of the call that wrote them
   uint64_t* bad = nullptr;  // [2]: non-finite sample sentinels (rows, cols)
   void* stage[2] = {nullptr, nullptr};  // pinned staging for pageable host buffers
   size_t stage_cap = 0;
@@ -74,6 +77,29 @@ struct Workspace {
     cap[slot] = bytes;
     return QK_OK;
   }
+  // as ensure(), but a fresh allocation is zeroed (arrival marks: 0 is never an epoch)
+  qk_status ensure_zeroed(int slot, size_t bytes) {
+    const bool grow = cap[slot] < bytes;
+    if (qk_status s = ensure(slot, bytes)) return s;
+    if (grow && bytes) {
+      cudaError_t e = cudaMemsetAsync(buf[slot], 0, cap[slot], stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess)
+        return set_error(QK_ERR_CUDA, std::string("flag reset: ") + cudaGetErrorString(e));
+    }
+    return QK_OK;
+  }
+  // next call epoch for the arrival marks (0 is reserved for "never written")
+  qk_status next_epoch() {
+    if (++epoch == 0) {
+      epoch = 1;
+      cudaError_t e = cudaMemsetAsync(buf[5], 0, cap[5], stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess)
+        return set_error(QK_ERR_CUDA, std::string("flag reset: ") + cudaGetErrorString(e));
+    }
+    return QK_OK;
+  }
 };
 
 Workspace g_ws[64];
@@ -91,6 +117,8 @@ qk_status workspace_for_current(Workspace** out, std::unique_lock<std::mutex>& l
     if (cudaError_t e = cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking))
       return cuda_err(e, "stream create");
     if (cudaError_t e = cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking))
+      return cuda_err(e, "stream create");
+    if (cudaError_t e = cudaStreamCreateWithFlags(&w->h2d_stream, cudaStreamNonBlocking))
       return cuda_err(e, "stream create");
     if (cudaError_t e = cudaMalloc(&w->bad, 2 * sizeof(uint64_t))) return cuda_err(e, "malloc");
     w->device = dev;
@@ -353,6 +381,106 @@ StreamWaitValue32Fn stream_wait_value32() {
   return fn;
 }
 
+typedef int (*StreamWriteValue32Fn)(cudaStream_t, uintptr_t, uint32_t, unsigned int);
+
+StreamWriteValue32Fn stream_write_value32() {
+  static StreamWriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return StreamWriteValue32Fn(nullptr);
+    }
+    return reinterpret_cast<StreamWriteValue32Fn>(p);
+  }();
+  return fn;
+}
+
+// In-kernel plane build for the host pipelines (L <= 2, pinned angle buffers, stream memory
+// operations available; QK_FUSED_BUILD=0 disables it): the angles go up in chunks of
+// kArriveBlocks plane blocks on w->h2d_stream, each followed by an arrival mark, and the
+// sweep starts at once — its CTAs build each plane block as soon as its chunk has landed, so
+// the H2D of the inputs overlaps the sweep instead of preceding it.
+bool fused_build_enabled(const Plan& p) {
+  static const bool on = [] {
+    const char* v = getenv("QK_FUSED_BUILD");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on && p.layers <= 2 && stream_write_value32() != nullptr &&
+         stream_wait_value32() != nullptr;
+}
+
+// Sets up set `k` of `fb` for n samples: build states in w->buf[4] at element offset
+// state_off, arrival marks in w->buf[5] at offset arr_off.
+void fused_set(Workspace* w, FusedBuild& fb, int k, const Plan& p, double* dX, int64_t n,
+               void* planes, int64_t state_off, int64_t arr_off, unsigned long long* bad) {
+  PlaneSrc& s = fb.set[k];
+  s.X = dX;
+  s.n = n;
+  s.ld = p.width;
+  s.planes = planes;
+  s.state = static_cast<int*>(w->buf[4]) + state_off;
+  s.arrived = static_cast<unsigned int*>(w->buf[5]) + arr_off;
+  s.epoch = w->epoch;
+  s.bad = bad;
+}
+
+// Enqueues the chunked H2D of set `k` on w->h2d_stream, each chunk followed by its arrival
+// mark.  Called right AFTER the sweep launch: the sweep waits for the marks, never the
+// reverse, and the host's enqueue time then overlaps the sweep's start.
+qk_status fused_h2d(Workspace* w, const PlaneSrc& s, const double* hX) {
+  const int64_t nb = blocks_for(s.n), pad = sample_pad(s.n);
+  StreamWriteValue32Fn write = stream_write_value32();
+  double* dX = const_cast<double*>(s.X);
+  unsigned int* arr = const_cast<unsigned int*>(s.arrived);
+  cudaError_t err = cudaSuccess;
+  for (int64_t c = 0; c * kArriveBlocks < nb; ++c) {
+    const int64_t s0 = std::max<int64_t>(0, c * kArriveBlocks * kTile - pad);
+    const int64_t s1 = std::min<int64_t>(s.n, (c + 1) * kArriveBlocks * kTile - pad);
+    if (s1 > s0 && err == cudaSuccess)
+      err = cudaMemcpyAsync(dX + s0 * s.ld, hX + s0 * s.ld, size_t(s1 - s0) * s.ld * sizeof(double),
+                            cudaMemcpyHostToDevice, w->h2d_stream);
+    // marks go out even after a failed copy so the running sweep can finish
+    if (write(w->h2d_stream, reinterpret_cast<uintptr_t>(arr + c), s.epoch, 0) != 0)
+      return set_error(QK_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+  return cuda_err(err, "H2D chunk");
+}
+
+int64_t arrive_chunks(int64_t n) { return (blocks_for(n) + kArriveBlocks - 1) / kArriveBlocks; }
+
+// Fused-build setup for up to two plane sets (set k: device angles dX[k], n[k] samples,
+// planes[k]); resets the build states and sentinels on w->stream.
+qk_status fused_setup(Workspace* w, const Plan& p, FusedBuild& fb, int n_sets, double* const* dX,
+                      const int64_t* n, void* const* planes) {
+  int64_t nb = 0, na = 0;
+  for (int k = 0; k < n_sets; ++k) {
+    nb += blocks_for(n[k]);
+    na += arrive_chunks(n[k]);
+  }
+  if (qk_status s = w->ensure(4, size_t(2 * nb + 2) * sizeof(int))) return s;  // + built counters
+  if (qk_status s = w->ensure_zeroed(5, size_t(std::max<int64_t>(na, 1)) * sizeof(unsigned)))
+    return s;
+  if (qk_status s = w->next_epoch()) return s;
+  if (cudaError_t e = cudaMemsetAsync(w->buf[4], 0, size_t(2 * nb + 2) * sizeof(int), w->stream))
+    return cuda_err(e, "build state reset");
+  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), w->stream))
+    return cuda_err(e, "sentinel reset");
+  int64_t so = 0, ao = 0;
+  for (int k = 0; k < n_sets; ++k) {
+    fused_set(w, fb, k, p, dX[k], n[k], planes[k], 2 * so, ao,
+              reinterpret_cast<unsigned long long*>(w->bad) + k);
+    fb.set[k].built = static_cast<int*>(w->buf[4]) + 2 * nb + k;
+    fb.set[k].nblocks = int(blocks_for(n[k]));
+    so += blocks_for(n[k]);
+    ao += arrive_chunks(n[k]);
+  }
+  if (n_sets == 1) fb.set[1] = fb.set[0];
+  return QK_OK;
+}
+
 // One row-major result matrix a sweep launch fills and the copy stream drains to the host.
 struct DrainTarget {
   double* d_K;
@@ -393,7 +521,8 @@ struct Trace {
 
 template <class Launch>
 qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targets,
-                        Launch&& launch, Trace* trace = nullptr) {
+                        Launch&& launch, Trace* trace = nullptr,
+                        const std::function<qk_status()>& after_launch = {}) {
   StreamWaitValue32Fn wait = stream_wait_value32();
   int64_t n_rows_total = 0;  // one counter per tile row
   bool all_pinned = true;
@@ -430,6 +559,14 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   if (qk_status s = launch()) {
     cudaEventDestroy(reset);
     return s;
+  }
+  if (after_launch) {
+    cudaStreamQuery(w->stream);  // the sweep is on its way; feed it
+    if (qk_status s = after_launch()) {
+      cudaStreamSynchronize(w->stream);  // a sweep waiting for missing chunks traps (20 s)
+      cudaEventDestroy(reset);
+      return s;
+    }
   }
   if (trace) trace->mark(3, w->stream);
   cudaStream_t cs = w->copy_stream;
@@ -576,19 +713,29 @@ qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int
   double* dX = static_cast<double*>(w->buf[0]);
   cudaStream_t st = w->stream;
   Trace trace(st);
-  if (qk_status s = upload(w, dX, h_angles, xb)) return s;
-  trace.mark(1, st);
-  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
-    return cuda_err(e, "sentinel reset");
-  if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
-  DrainTarget tg[1] = {{static_cast<double*>(w->buf[2]), h_K, N, N, kModeGram, nullptr}};
   void* planes = w->buf[1];
+  const bool fused = fused_build_enabled(*p) && is_pinned(h_angles);
+  FusedBuild fb;
+  if (fused) {
+    if (qk_status s = fused_setup(w, *p, fb, 1, &dX, &N, &planes)) return s;
+    trace.mark(1, st);
+  } else {
+    if (qk_status s = upload(w, dX, h_angles, xb)) return s;
+    trace.mark(1, st);
+    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
+      return cuda_err(e, "sentinel reset");
+    if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
+  }
+  DrainTarget tg[1] = {{static_cast<double*>(w->buf[2]), h_K, N, N, kModeGram, nullptr}};
   if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
         return launch_sweep(*p, kModeGram, planes, N, planes, N, 0,
                             qk_gram_tile_count(plan, N), tg[0].d_K, N, QK_OUT_DENSE, w->stream,
-                            tg[0].d_prog);
-      }, &trace))
+                            tg[0].d_prog, fused ? &fb : nullptr);
+      }, &trace, fused ? std::function<qk_status()>([&] { return fused_h2d(w, fb.set[0], h_angles); })
+                       : std::function<qk_status()>()))
     return s;
+  if (fused)
+    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
   static const char* const names[1] = {"train"};
   return check_bad(w->bad, 1, names);
 }
@@ -616,21 +763,37 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   char* dPc = dPr + prb;
   cudaStream_t st = w->stream;
   Trace trace(st);
-  if (qk_status s = upload(w, dXr, h_rows, xrb)) return s;
-  if (qk_status s = upload(w, dXc, h_cols, xcb)) return s;
-  trace.mark(1, st);
-  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
-    return cuda_err(e, "sentinel reset");
-  if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
-  if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st)) return s;
+  const bool fused = fused_build_enabled(*p) && is_pinned(h_rows) && is_pinned(h_cols);
+  FusedBuild fb;
+  if (fused) {
+    double* dXs[2] = {dXr, dXc};
+    const int64_t ns[2] = {n_rows, n_cols};
+    void* ps[2] = {dPr, dPc};
+    if (qk_status s = fused_setup(w, *p, fb, 2, dXs, ns, ps)) return s;
+    trace.mark(1, st);
+  } else {
+    if (qk_status s = upload(w, dXr, h_rows, xrb)) return s;
+    if (qk_status s = upload(w, dXc, h_cols, xcb)) return s;
+    trace.mark(1, st);
+    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+      return cuda_err(e, "sentinel reset");
+    if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
+    if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st))
+      return s;
+  }
   DrainTarget tg[1] = {
       {static_cast<double*>(w->buf[2]), h_K, n_rows, n_cols, kModeCross, nullptr}};
   if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
         return launch_sweep(*p, kModeCross, dPr, n_rows, dPc, n_cols, 0,
                             qk_cross_tile_count(plan, n_rows, n_cols), tg[0].d_K, n_cols,
-                            QK_OUT_DENSE, w->stream, tg[0].d_prog);
-      }, &trace))
+                            QK_OUT_DENSE, w->stream, tg[0].d_prog, fused ? &fb : nullptr);
+      }, &trace, fused ? std::function<qk_status()>([&]() -> qk_status {
+        if (qk_status s = fused_h2d(w, fb.set[1], h_cols)) return s;  // train (cols) first
+        return fused_h2d(w, fb.set[0], h_rows);
+      }) : std::function<qk_status()>()))
     return s;
+  if (fused)
+    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
   static const char* const names[2] = {"test", "train"};
   return check_bad(w->bad, 2, names);
 }
@@ -664,21 +827,39 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
   double* dKs = dKt + size_t(n_train) * size_t(n_train);
   cudaStream_t st = w->stream;
   Trace trace(st);
-  if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
-  if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
-  trace.mark(1, st);
-  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
-    return cuda_err(e, "sentinel reset");
-  if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
-  if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st)) return s;
+  const bool fused = fused_build_enabled(*p) && is_pinned(h_train) &&
+                     (n_test == 0 || is_pinned(h_test));
+  FusedBuild fb;
+  if (fused) {
+    double* dXs2[2] = {dXt, dXs};
+    const int64_t ns[2] = {n_train, n_test};
+    void* ps[2] = {dPt, dPs};
+    if (qk_status s = fused_setup(w, *p, fb, n_test > 0 ? 2 : 1, dXs2, ns, ps)) return s;
+    trace.mark(1, st);
+  } else {
+    if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
+    if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
+    trace.mark(1, st);
+    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+      return cuda_err(e, "sentinel reset");
+    if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
+    if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
+      return s;
+  }
   DrainTarget tg[2] = {{dKt, h_K_train, n_train, n_train, kModeGram, nullptr},
                        {dKs, h_K_cross, n_test, n_train, kModeCross, nullptr}};
   const int64_t nt = qk_job_tile_count(plan, n_train, n_test);
   if (qk_status s = run_and_drain(w, *p, tg, n_test > 0 ? 2 : 1, [&] {
         return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
-                          tg[1].d_prog);
-      }, &trace))
+                          tg[1].d_prog, fused ? &fb : nullptr);
+      }, &trace, fused ? std::function<qk_status()>([&]() -> qk_status {
+        if (qk_status s = fused_h2d(w, fb.set[0], h_train)) return s;
+        return n_test > 0 ? fused_h2d(w, fb.set[1], h_test) : QK_OK;
+      }) : std::function<qk_status()>()))
     return s;
+  if (fused) print_fused_stats(148);
+  if (fused)
+    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
   static const char* const names[2] = {"train", "test"};
   return check_bad(w->bad, 2, names);
 }

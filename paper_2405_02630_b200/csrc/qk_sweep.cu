@@ -21,7 +21,10 @@
 // For L = 1 the amplitude is prod_q cos((x_j - x_i)/2) from half-angle planes.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 
@@ -437,28 +440,31 @@ __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows,
 // ------------------------------------------------------------------------------------------
 // Gate build: angles -> planes[block][q][t] = (cos x, sin x)  (L = 2)  or  half angles (L != 2)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) gate_build_kernel(const double* __restrict__ X,
-                                                         int64_t n_samples, int64_t ld,
-                                                         int width, int n_pad, int front,
-                                                         int half, double2* __restrict__ planes,
-                                                         unsigned long long* bad) {
-  __shared__ double tile[kTile][33];
-  const int64_t blk = blockIdx.x;
-  const int q0 = blockIdx.y * 32;
+// One 64-sample x 32-qubit slab of plane block `blk`: coalesced angle reads into a shared
+// transpose tile, then coalesced plane writes (qubit-major).  `tile` is 64 x 33 doubles.
+// Shared by the gate-build kernel and the sweep's in-kernel builder (bit-identical planes).
+// CG: read the angles through L2 only (the in-kernel builder reads angles that a copy engine
+// wrote during the same launch).
+template <bool CG, int QS>
+__device__ __forceinline__ void build_plane_slab(const double* __restrict__ X, int64_t n_samples,
+                                                 int64_t ld, int width, int n_pad, int front,
+                                                 int half, double2* __restrict__ planes,
+                                                 unsigned long long* bad, int64_t blk, int q0,
+                                                 double (*tile)[QS + 1]) {
   const int spad = sample_pad(n_samples);
-  for (int idx = threadIdx.x; idx < kTile * 32; idx += blockDim.x) {
-    const int t = idx >> 5, qq = idx & 31;
+  for (int idx = threadIdx.x; idx < kTile * QS; idx += blockDim.x) {
+    const int t = idx / QS, qq = idx % QS;
     const int64_t s = blk * kTile + t - spad;  // padding slots (s < 0) get angle 0
     const int q = q0 + qq - front;
     double x = 0.0;
     if (s >= 0 && s < n_samples && q >= 0 && q < width) {
-      x = __ldg(X + s * ld + q);
+      x = CG ? __ldcg(X + s * ld + q) : __ldg(X + s * ld + q);
       if (bad != nullptr && !isfinite(x)) atomicMin(bad, (unsigned long long)s);
     }
     tile[t][qq] = x;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < kTile * 32; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < kTile * QS; idx += blockDim.x) {
     const int qq = idx >> 6, t = idx & 63;
     const int q = q0 + qq;
     if (q >= n_pad) break;
@@ -467,6 +473,16 @@ __global__ void __launch_bounds__(256) gate_build_kernel(const double* __restric
     sincos(half ? 0.5 * x : x, &sn, &cs);
     planes[(blk * n_pad + q) * kTile + t] = make_double2(cs, sn);
   }
+}
+
+__global__ void __launch_bounds__(256) gate_build_kernel(const double* __restrict__ X,
+                                                         int64_t n_samples, int64_t ld,
+                                                         int width, int n_pad, int front,
+                                                         int half, double2* __restrict__ planes,
+                                                         unsigned long long* bad) {
+  __shared__ double tile[kTile][33];
+  build_plane_slab<false, 32>(X, n_samples, ld, width, n_pad, front, half, planes, bad,
+                              blockIdx.x, blockIdx.y * 32, tile);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -499,7 +515,99 @@ struct SweepArgs {
   double* out2;
   unsigned int* progress2;
   int pad_rows, pad_cols, pad_rows2;  // sample_pad() of each plane set (front of block 0)
+  // In-kernel plane build (fused = 1): the plane blocks of rows / cols / rows2 are built by
+  // the sweep's own CTAs from src[set_*] as their angles arrive (see ensure_block).
+  int fused, width, half;
+  int set_rows, set_cols, set_rows2;
+  PlaneSrc src[2];
+  unsigned long long* stats;  // diagnostics (QK_FUSED_STATS=1): per CTA ns in ensure, t0, t_end
+  unsigned long long* next_tile;  // dynamic tile claims beyond the first wave (zeroed per launch)
 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void add_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
+
+// CTA-wide (every thread calls it; it ends on a barrier): make plane block b of `ps` exist.
+// A block is built in 64-qubit slabs that any CTA needing the block claims one at a time
+// (state[2b]: slabs claimed, state[2b+1]: slabs built), so the CTAs that reach a new block
+// together build it together.  Building needs the block's angles: the host stream writes the
+// call's epoch into arrived[b / kArriveBlocks] after each chunk of the H2D.  With `wait` the
+// CTA waits for the angles and then for the block to be complete; without (look-ahead: the
+// block is needed a tile later) it only claims slabs of a block whose angles have landed and
+// never waits.  A CTA never waits while holding an unbuilt claim, so this cannot deadlock;
+// a 20 s guard traps instead of hanging if an arrival never comes.
+__device__ __noinline__ void ensure_block(const PlaneSrc ps, int64_t b, int n_pad, int front,
+                                          int width, int half, double (*tile)[64 + 1], int* flag,
+                                          bool wait, unsigned long long* build_ns) {
+  const int nslabs = (n_pad + 63) / 64;
+  int* claimed = ps.state + 2 * b;
+  int* done = claimed + 1;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      int slab = -1;
+      if (ld_acquire_gpu(done) < nslabs) {
+        const unsigned long long t0 = global_ns();
+        const unsigned int* arr = ps.arrived + b / kArriveBlocks;
+        bool ready = ld_acquire_sys(arr) == ps.epoch;
+        while (wait && !ready) {
+          __nanosleep(256);
+          if (global_ns() - t0 > 20000000000ull) __trap();
+          ready = ld_acquire_sys(arr) == ps.epoch;
+        }
+        if (ready && *(volatile int*)claimed < nslabs) {
+          const int k = atomicAdd(claimed, 1);
+          if (k < nslabs) slab = k;
+        }
+        if (slab < 0 && wait) {
+          while (ld_acquire_gpu(done) < nslabs) {
+            __nanosleep(256);
+            if (global_ns() - t0 > 20000000000ull) __trap();
+          }
+        }
+      }
+      *flag = slab;
+    }
+    __syncthreads();
+    const int slab = *flag;
+    if (slab < 0) break;
+    const unsigned long long tb = build_ns ? global_ns() : 0;
+    build_plane_slab<true, 64>(ps.X, ps.n, ps.ld, width, n_pad, front, half,
+                               static_cast<double2*>(ps.planes), ps.bad, b, slab * 64, tile);
+    __threadfence();
+    __syncthreads();  // the slab is written; the transpose tile and `flag` are free
+    if (threadIdx.x == 0) {
+      if (add_acq_rel_gpu(done, 1) == nslabs - 1) add_release_gpu(ps.built, 1);
+      if (build_ns) build_ns[0] += global_ns() - tb, build_ns[1] += 1;
+    }
+  }
+  __syncthreads();  // `flag` is reused by the next call
+}
 
 // Per-tile coordinates: tile rows/cols in plane blocks and which problem of a kModeJob launch.
 struct TileXY {
@@ -507,7 +615,7 @@ struct TileXY {
   int prob;
 };
 
-template <int LAYERS, int MODE, int OUT, int RI>
+template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
 __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
   using St = typename BondT<LAYERS>::type;
   constexpr int kRI = Geo<RI>::kRI, kWarps = Geo<RI>::kWarps;
@@ -518,41 +626,114 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
 
   const int tid = threadIdx.x;
   const int lane = tid % 32;
-  const int64_t my_tiles =
-      a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nchunks = a.nchunks;
-  const int64_t F = my_tiles * nchunks;
 
+  // Dynamic tile schedule: CTA b starts with tile b; every further tile is claimed from a
+  // launch-wide counter (tiles gridDim.x, gridDim.x + 1, ... in list order), so CTAs that
+  // spend time elsewhere (plane builds, cheaper padding tiles) simply take fewer tiles.  The
+  // chunks of a CTA's tile k + kLook are issued during tile k, so tile k + kLook is claimed
+  // (thread 0) at the start of tile k and published by a CTA barrier.  Claims live in a small
+  // shared ring indexed by the CTA-local tile number.
+  const int kLook = 1 + (kStages - 1) / nchunks;
+  struct Claim {
+    int64_t g;  // launch-local tile index (>= n_tiles: none)
+    int bi, bj, prob;
+  };
+  __shared__ Claim ring[8];
   int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
   double* stage_T = reinterpret_cast<double*>(table + kTileTable);  // epilogue staging tile
-  auto decode = [&](int64_t k) -> TileXY {
-    const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
-    TileXY t;
-    t.prob = 0;
-    if (MODE == kModeGram || (MODE == kModeJob && g < a.n_first)) {
-      decode_upper(g, a.nb_rows, t.bi, t.bj);
-    } else if (MODE == kModeCross) {
-      decode_rect(g, a.nb_rows, a.nb_cols, t.bi, t.bj);
-    } else {
-      decode_rect(g - a.n_first, a.nb_rows2, a.nb_cols, t.bi, t.bj);
-      t.prob = 1;
+  auto claim = [&](int64_t k) {  // thread 0 only
+    Claim c;
+    c.g = k == 0 ? int64_t(blockIdx.x)
+                 : int64_t(gridDim.x) + int64_t(atomicAdd(a.next_tile, 1ull));
+    c.bi = c.bj = c.prob = 0;
+    if (c.g < a.n_tiles) {
+      const int64_t g = a.tile_begin + c.g;
+      int64_t bi, bj;
+      if (MODE == kModeGram || (MODE == kModeJob && g < a.n_first)) {
+        decode_upper(g, a.nb_rows, bi, bj);
+      } else if (MODE == kModeCross) {
+        decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+      } else {
+        decode_rect(g - a.n_first, a.nb_rows2, a.nb_cols, bi, bj);
+        c.prob = 1;
+      }
+      c.bi = int(bi);
+      c.bj = int(bj);
     }
-    return t;
+    ring[k & 7] = c;
   };
+  auto valid = [&](int64_t k) { return ring[k & 7].g < a.n_tiles; };
   auto tile_of = [&](int64_t k) -> TileXY {
-    if (k < kTileTable) {
-      const int2 e = table[k];
-      return TileXY{e.x & 0x3fffffff, e.y, e.x >> 30};
-    }
-    return decode(k);
+    const Claim& c = ring[k & 7];
+    return TileXY{c.bi, c.bj, c.prob};
   };
-  for (int64_t k = tid; k < my_tiles && k < kTileTable; k += blockDim.x) {
-    const TileXY t = decode(k);
-    table[k] = make_int2(int(t.bi) | (t.prob << 30), int(t.bj));
-  }
+  if (tid == 0)
+    for (int64_t k = 0; k <= kLook; ++k) claim(k);
   __syncthreads();
-  auto issue = [&](int64_t f) {  // fill stage f % kStages with item f
+  // fused plane build: tiles whose chunks may be issued before the next ensure point.  Once
+  // this CTA has seen every block of a set built (one acquire of the set's counter, then one
+  // proxy fence), tiles of that set need no check, barrier or fence.
+  __shared__ int build_flag;
+  __shared__ int set_done[2];
+  if (FUSED && tid == 0) set_done[0] = set_done[1] = 0;
+  if (FUSED) __syncthreads();
+  int64_t ensured = -1;
+  unsigned long long st_ns = 0, st_t0 = FUSED && a.stats ? global_ns() : 0, st_first = 0;
+  __shared__ unsigned long long bstat_s[2];
+  unsigned long long* bstat = nullptr;
+  if (FUSED && a.stats) {
+    if (tid == 0) bstat_s[0] = bstat_s[1] = 0;
+    bstat = bstat_s;
+  }
+  auto ensure_upto = [&](int64_t last, bool lookahead) {
+    while (last > ensured && !valid(last)) --last;  // claims past the end of the list
+    bool need = false;
+    for (int64_t k = ensured + 1; k <= last; ++k) {
+      const TileXY t = tile_of(k);
+      need |= !set_done[t.prob ? a.set_rows2 : a.set_rows] || !set_done[a.set_cols];
+    }
+    if (!need) {
+      ensured = last > ensured ? last : ensured;
+      return;
+    }
+    __syncthreads();  // every warp is past the previous epilogue (stage_T is the build tile)
+    const unsigned long long e0 = a.stats ? global_ns() : 0;
+    double (*tile)[65] = reinterpret_cast<double (*)[65]>(stage_T);
+    for (; ensured < last;) {
+      const TileXY t = tile_of(++ensured);
+      const int si = t.prob ? a.set_rows2 : a.set_rows;
+      if (!set_done[si])
+        ensure_block(si ? a.src[1] : a.src[0], t.bi, a.n_pad, a.front, a.width, a.half, tile,
+                     &build_flag, true, bstat);
+      if (!set_done[a.set_cols])
+        ensure_block(a.set_cols ? a.src[1] : a.src[0], t.bj, a.n_pad, a.front, a.width, a.half,
+                     tile, &build_flag, true, bstat);
+    }
+    if (lookahead && valid(last + 1)) {  // build (never wait for) the next tile's blocks
+      const TileXY t = tile_of(last + 1);
+      const int si = t.prob ? a.set_rows2 : a.set_rows;
+      if (!set_done[si])
+        ensure_block(si ? a.src[1] : a.src[0], t.bi, a.n_pad, a.front, a.width, a.half, tile,
+                     &build_flag, false, bstat);
+      if (!set_done[a.set_cols])
+        ensure_block(a.set_cols ? a.src[1] : a.src[0], t.bj, a.n_pad, a.front, a.width, a.half,
+                     tile, &build_flag, false, bstat);
+    }
+    if (tid == 0) {
+      if (!set_done[0] && ld_acquire_gpu(a.src[0].built) == a.src[0].nblocks) set_done[0] = 1;
+      if (!set_done[1] && ld_acquire_gpu(a.src[1].built) == a.src[1].nblocks) set_done[1] = 1;
+    }
+    // the planes were written through the generic proxy; the bulk copies read them through
+    // the async proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();  // set_done
+    if (a.stats) st_ns += global_ns() - e0;
+  };
+  if constexpr (FUSED) ensure_upto((kStages - 1) / nchunks, false);
+  auto issue = [&](int64_t f) {  // fill stage f % kStages with item f (if its tile exists)
     const int64_t k = f / nchunks;
+    if (!valid(k)) return;
     const int c = int(f - k * nchunks);
     const TileXY t = tile_of(k);
     const int stage = int(f % kStages);
@@ -571,7 +752,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       released[s] = 0;
     }
     fence_mbar_init();
-    for (int64_t f = 0; f < F && f < kStages; ++f) issue(f);
+    for (int64_t f = 0; f < kStages; ++f) issue(f);
   }
   __syncthreads();
 
@@ -582,7 +763,17 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   const int warp_row_end = (tid / 32 + 1) * (32 / kTX) * kRI;  // rows [.., end) of this warp
   St st[kRI][kRJ];
   int64_t f = 0;
-  for (int64_t k = 0; k < my_tiles; ++k) {
+  for (int64_t k = 0; valid(k); ++k) {
+    if (k > 0) {  // claim tile k + kLook (its chunks are issued during tile k)
+      if (tid == 0) claim(k + kLook);
+      __syncthreads();
+    }
+    // fused build: the blocks of tile k + 1 are needed once its first chunks are issued
+    // (during tile k); ensure them here, where no bond state is live
+    if constexpr (FUSED) {
+      ensure_upto(k + 1 + (kStages - 1) / nchunks, true);
+      if (k == 0 && a.stats) st_first = global_ns();
+    }
     const TileXY tk = tile_of(k);
     // padding rows of this tile (front of plane block 0): warps made only of them skip the
     // sweep (they still release every stage) — the ragged sample block costs ~1/4 of a tile
@@ -627,7 +818,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         // the last warp to release the stage refills it with item f + kStages
         if (atomicAdd(&released[stage], 1) == kWarps - 1) {
           released[stage] = 0;
-          if (f + kStages < F) issue(f + kStages);
+          issue(f + kStages);
         }
       }
       if (LAYERS == 2 && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0) {
@@ -643,8 +834,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     const int64_t bi = t.bi, bj = t.bj;
     const bool gram = MODE == kModeGram || (MODE == kModeJob && t.prob == 0);
     if (OUT == QK_OUT_PACKED) {
-      const int64_t g = a.tile_begin + blockIdx.x + k * gridDim.x;
-      double* o = a.out + (g - a.tile_begin) * int64_t(kTile * kTile);
+      double* o = a.out + ring[k & 7].g * int64_t(kTile * kTile);
 #pragma unroll
       for (int r = 0; r < kRI; ++r)
 #pragma unroll
@@ -741,6 +931,16 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       QK_PROGRESS_FENCE();
       __syncthreads();
       if (tid == 0) atomicAdd(prog + bi, 1u);  // per tile row
+    }
+  }
+  if constexpr (FUSED) {
+    if (a.stats != nullptr && tid == 0) {
+      a.stats[6 * blockIdx.x] = st_ns;
+      a.stats[6 * blockIdx.x + 1] = st_t0;
+      a.stats[6 * blockIdx.x + 2] = global_ns();
+      a.stats[6 * blockIdx.x + 3] = bstat_s[0];
+      a.stats[6 * blockIdx.x + 4] = bstat_s[1];
+      a.stats[6 * blockIdx.x + 5] = st_first;
     }
   }
 }
@@ -1118,9 +1318,31 @@ qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, in
   return cuda_status(cudaGetLastError(), "gate_build launch");
 }
 
-template <int LAYERS, int MODE, int OUT, int RI>
-static qk_status launch_sweep_ri(const SweepArgs& a, cudaStream_t st) {
-  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI>;
+// Per-launch tile-claim counters (the dynamic schedule): a ring of zeroed 8-byte slots per
+// device, one per launch, so concurrent launches on different streams never share one.
+static qk_status tile_counter(cudaStream_t st, unsigned long long** out) {
+  constexpr int kSlots = 4096;
+  static unsigned long long* pool[64] = {};
+  static std::mutex mu;
+  static std::atomic<uint64_t> seq{0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_status(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return set_error(QK_ERR_CUDA, "device index out of range");
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (pool[dev] == nullptr)
+      if (cudaError_t e = cudaMalloc(&pool[dev], kSlots * sizeof(unsigned long long)))
+        return cuda_status(e, "tile counter allocation");
+  }
+  *out = pool[dev] + (seq.fetch_add(1) % kSlots);
+  return cuda_status(cudaMemsetAsync(*out, 0, sizeof(unsigned long long), st),
+                     "tile counter reset");
+}
+
+template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
+static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
+  if (qk_status s = tile_counter(st, &a.next_tile)) return s;
+  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI, FUSED>;
   constexpr int threads = Geo<RI>::kThreads;
   // per call: the attribute is per device and costs microseconds
   cudaError_t e =
@@ -1150,8 +1372,14 @@ static int sweep_ri() {
 
 template <int LAYERS, int MODE, int OUT>
 static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
-  if (sweep_ri() == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2>(a, st);
-  return launch_sweep_ri<LAYERS, MODE, OUT, 4>(a, st);
+  if constexpr (OUT == QK_OUT_DENSE) {  // the in-kernel plane build serves the host pipelines
+    if (a.fused) {
+      if (sweep_ri() == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, true>(a, st);
+      return launch_sweep_ri<LAYERS, MODE, OUT, 4, true>(a, st);
+    }
+  }
+  if (sweep_ri() == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, false>(a, st);
+  return launch_sweep_ri<LAYERS, MODE, OUT, 4, false>(a, st);
 }
 
 template <int LAYERS, int MODE, int OUT>
@@ -1210,12 +1438,66 @@ static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, 
   return cuda_status(cudaGetLastError(), "deep pairs launch");
 }
 
+// QK_FUSED_STATS=1 (diagnostics): per-CTA time spent building / waiting for plane blocks,
+// printed after each fused launch.
+static unsigned long long* fused_stats() {
+  static unsigned long long* buf = [] {
+    const char* v = getenv("QK_FUSED_STATS");
+    unsigned long long* b = nullptr;
+    if (v != nullptr && v[0] == '1' && cudaMallocManaged(&b, 6 * 4096 * 8) != cudaSuccess) b = nullptr;
+    return b;
+  }();
+  return buf;
+}
+
+void print_fused_stats(int grid) {
+  unsigned long long* s = fused_stats();
+  if (s == nullptr) return;
+  cudaDeviceSynchronize();
+  unsigned long long t0 = ~0ull, t1 = 0, mx = 0, sum = 0, bsum = 0, bn = 0, bmx = 0, fmx = 0;
+  unsigned long long first_end = ~0ull;
+  for (int b = 0; b < grid; ++b) t0 = std::min(t0, s[6 * b + 1]);
+  for (int b = 0; b < grid; ++b) {
+    t1 = std::max(t1, s[6 * b + 2]);
+    first_end = std::min(first_end, s[6 * b + 2]);
+    mx = std::max(mx, s[6 * b]);
+    sum += s[6 * b];
+    bsum += s[6 * b + 3];
+    bn += s[6 * b + 4];
+    bmx = std::max(bmx, s[6 * b + 3]);
+    fmx = std::max(fmx, s[6 * b + 5] - t0);
+  }
+  fprintf(stderr,
+          "qk_fused_stats kernel %.3f ms, ensure max %.3f mean %.3f ms, builds %llu (%.1f us "
+          "each, max per CTA %.3f ms), first tile by %.3f ms, CTA ends %.3f..%.3f ms\n",
+          (t1 - t0) * 1e-6, mx * 1e-6, sum * 1e-6 / grid, bn, bn ? bsum * 1e-3 / bn : 0.0,
+          bmx * 1e-6, fmx * 1e-6, (first_end - t0) * 1e-6, (t1 - t0) * 1e-6);
+}
+
+static void set_fused(SweepArgs& a, const Plan& p, const FusedBuild* fb, int rows, int cols,
+                      int rows2) {
+  if (fb == nullptr || p.layers > 2) return;  // L >= 3 kernels read prebuilt planes
+  a.stats = fused_stats();
+  a.fused = 1;
+  a.width = p.width;
+  a.half = p.layers == 2 ? 0 : 1;
+  a.src[0] = fb->set[0];
+  a.src[1] = fb->set[1];
+  a.set_rows = rows;
+  a.set_cols = cols;
+  a.set_rows2 = rows2;
+}
+
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress) {
+                       unsigned int* d_progress, const FusedBuild* fused) {
   if (tile_end <= tile_begin) return QK_OK;
+  if (fused != nullptr && p.layers > 2)
+    return set_error(QK_ERR_VALUE, "in-kernel plane build needs layers <= 2");
   SweepArgs a{};
+  if (mode == kModeGram) set_fused(a, p, fused, 0, 0, 0);
+  else set_fused(a, p, fused, 0, 1, 0);
   a.progress = d_progress;
   a.rows = static_cast<const double2*>(d_rows);
   a.cols = static_cast<const double2*>(d_cols);
@@ -1274,22 +1556,33 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train,
-                     unsigned int* d_prog_cross) {
+                     unsigned int* d_prog_cross, const FusedBuild* fused) {
   if (tile_end <= tile_begin) return QK_OK;
+  if (fused != nullptr && p.layers > 2)
+    return set_error(QK_ERR_VALUE, "in-kernel plane build needs layers <= 2");
   const int64_t nbt = blocks_for(n_train);
   const int64_t n_gram = nbt * (nbt + 1) / 2;
   if (p.layers >= 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
     // one problem only (or the one-pair-per-thread L >= 3 kernel): plain launches
+    FusedBuild gram_fb, cross_fb;
+    if (fused != nullptr) {
+      gram_fb.set[0] = gram_fb.set[1] = fused->set[0];
+      cross_fb.set[0] = fused->set[1];  // cross: [0] rows (test), [1] cols (train)
+      cross_fb.set[1] = fused->set[0];
+    }
     if (qk_status s = launch_sweep(p, kModeGram, d_train, n_train, d_train, n_train, tile_begin,
                                    std::min(tile_end, n_gram), d_K_train, n_train,
-                                   QK_OUT_DENSE, stream, d_prog_train))
+                                   QK_OUT_DENSE, stream, d_prog_train,
+                                   fused ? &gram_fb : nullptr))
       return s;
     if (n_test == 0 || tile_end <= n_gram) return QK_OK;
     return launch_sweep(p, kModeCross, d_test, n_test, d_train, n_train,
                         std::max(tile_begin, n_gram) - n_gram, tile_end - n_gram, d_K_cross,
-                        n_train, QK_OUT_DENSE, stream, d_prog_cross);
+                        n_train, QK_OUT_DENSE, stream, d_prog_cross,
+                        fused ? &cross_fb : nullptr);
   }
   SweepArgs a{};
+  set_fused(a, p, fused, 0, 0, 1);
   a.rows = static_cast<const double2*>(d_train);
   a.cols = static_cast<const double2*>(d_train);
   a.n_rows = n_train;

@@ -1,0 +1,30 @@
+"""Host-pipeline phase timing (QK_TRACE=1 prints h2d / gate / sweep / tail / host per call):
+config 4 (10,000 x 784 train, 2,000 test) through compute_kernel_matrices with pinned
+buffers.  usage: QK_TRACE=1 [QK_FUSED_BUILD=0] python tools/e2e_trace.py [calls]"""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2405_02630_b200 import FeatureMapConfig, compute_kernel_matrices  # noqa: E402
+
+
+def pin(a):
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+    t[...] = a
+    return t
+
+
+rng = np.random.default_rng(0)
+X = pin(rng.uniform(0, np.pi, (10000, 784)))
+T = pin(rng.uniform(0, np.pi, (2000, 784)))
+K = pin(np.empty((10000, 10000)))
+Kx = pin(np.empty((2000, 10000)))
+cfg = FeatureMapConfig(784)
+for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 4):
+    t = time.perf_counter()
+    compute_kernel_matrices(X, T, cfg, out_train=K, out_test=Kx)
+    print(f"wall {(time.perf_counter() - t) * 1e3:.3f} ms", flush=True)
