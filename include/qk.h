@@ -172,6 +172,14 @@ qk_status qk_shared_free(void* d_ptr);
 qk_status qk_ipc_export(const void* d_ptr, unsigned char out_handle[QK_IPC_HANDLE_BYTES]);
 qk_status qk_ipc_import(const unsigned char handle[QK_IPC_HANDLE_BYTES], void** out_d_ptr);
 qk_status qk_ipc_close(void* d_ptr);
+/* Host side of the multi-GPU result: a row-major host matrix that every rank process maps
+ * (a POSIX shared-memory segment) is page-locked in each of them (qk_host_register), and
+ * each rank copies ITS row slice of rank 0's device matrix into it (qk_copy_d2h: a
+ * stream-ordered copy from any device address, peer memory included), so the 8 B/entry
+ * result crosses N PCIe links in parallel instead of rank 0's alone. */
+qk_status qk_host_register(void* h_ptr, size_t bytes);
+qk_status qk_host_unregister(void* h_ptr);
+qk_status qk_copy_d2h(void* h_dst, const void* d_src, size_t bytes, void* stream);
 
 /* ---- dense state-vector ground truth (checker beyond the reference's 24-qubit guard) ----
  * Replaces the reference's brute-force simulator (statevector.py:41-70, simulate /

@@ -931,4 +931,22 @@ qk_status qk_ipc_close(void* d_ptr) {
   return cuda_err(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
 }
 
+qk_status qk_host_register(void* h_ptr, size_t bytes) {
+  if (h_ptr == nullptr || bytes == 0) return set_error(QK_ERR_VALUE, "empty host range");
+  return cuda_err(cudaHostRegister(h_ptr, bytes, cudaHostRegisterPortable), "cudaHostRegister");
+}
+
+qk_status qk_host_unregister(void* h_ptr) {
+  if (h_ptr == nullptr) return QK_OK;
+  return cuda_err(cudaHostUnregister(h_ptr), "cudaHostUnregister");
+}
+
+qk_status qk_copy_d2h(void* h_dst, const void* d_src, size_t bytes, void* stream) {
+  if (bytes == 0) return QK_OK;
+  if (h_dst == nullptr || d_src == nullptr) return set_error(QK_ERR_VALUE, "NULL pointer");
+  return cuda_err(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost,
+                                  static_cast<cudaStream_t>(stream)),
+                  "D2H copy");
+}
+
 }  // extern "C"

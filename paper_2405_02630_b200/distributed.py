@@ -15,6 +15,11 @@ sweeps its range.  Two ways to land the results on rank 0:
 * ``placement="gather"``: packed tiles padded to the common range length, one ``gather`` to
   rank 0 (NCCL), then the unpack kernel.  For fabrics without peer access.
 
+Host buffers (``KernelJob.run_host``): the inputs go up per rank, the p2p job runs, and each
+rank then copies ITS row slice of rank 0's matrices into a host matrix every rank maps
+(:class:`SharedHostMatrix`, a POSIX shared-memory segment page-locked in each process), so
+the 8 B/entry result leaves the GPUs over N PCIe links in parallel.
+
 World size 1 writes the dense matrices directly.  The partition / placement logic is
 device-agnostic (tested with gloo on CPU); the p2p path is tested with two processes sharing
 one GPU (CUDA IPC works within a device), the sweeps/unpacks by the GPU parity tests.
@@ -24,6 +29,9 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 from math import ceil
+from multiprocessing import shared_memory
+
+import numpy as np
 
 import torch
 import torch.distributed as dist
@@ -139,6 +147,92 @@ class SharedMatrix:
             lib = _native._lib
             (lib.qk_shared_free if self.owner else lib.qk_ipc_close)(self.ptr)
         self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+class SharedHostMatrix:
+    """Row-major fp64 host matrix shared by the rank processes of one node: a POSIX
+    shared-memory segment (or, when /dev/shm is too small for it, a file under the temp
+    directory mapped MAP_SHARED) that rank 0 creates (``name=None``) and the others attach by
+    name, page-locked in every process (``qk_host_register``) so each rank's copy engine can
+    DMA its slice of the result into it.  ``array`` is the numpy view."""
+
+    def __init__(self, rows: int, cols: int, name: str | None = None):
+        import mmap
+        import os
+        import tempfile
+
+        self.rows, self.cols = int(rows), int(cols)
+        nbytes = max(8, self.rows * self.cols * 8)
+        self.owner = name is None
+        self._shm = self._file = None
+        if self.owner:
+            try:
+                st = os.statvfs("/dev/shm")
+                use_shm = st.f_bavail * st.f_frsize >= nbytes + (64 << 20)
+            except OSError:
+                use_shm = False
+            if use_shm:
+                self._shm = shared_memory.SharedMemory(create=True, size=nbytes)
+                self.name = "shm:" + self._shm.name
+            else:
+                fd, path = tempfile.mkstemp(prefix="qk_host_", suffix=".f64")
+                os.ftruncate(fd, nbytes)
+                self._file = (fd, path)
+                self.name = "file:" + path
+        else:
+            kind, _, ident = name.partition(":")
+            if kind == "shm":
+                self._shm = shared_memory.SharedMemory(name=ident, create=False)
+                try:  # the creator unlinks it; keep this process's tracker out of it
+                    from multiprocessing import resource_tracker
+                    resource_tracker.unregister(self._shm._name, "shared_memory")
+                except Exception:  # pragma: no cover - tracker internals differ
+                    pass
+            else:
+                self._file = (os.open(ident, os.O_RDWR), ident)
+            self.name = name
+        if self._shm is not None:
+            buf = self._shm.buf
+        else:
+            self._map = mmap.mmap(self._file[0], nbytes, flags=mmap.MAP_SHARED)
+            buf = self._map
+        self.array = np.ndarray((self.rows, self.cols), dtype=np.float64, buffer=buf)
+        self._ptr = self.array.ctypes.data
+        self._nbytes = nbytes
+        _native.bind_current_device()
+        _native.check(_native.lib().qk_host_register(self._ptr, nbytes))
+        self._registered = True
+
+    def close(self) -> None:
+        import os
+
+        if getattr(self, "_registered", False) and _native._lib is not None:
+            _native._lib.qk_host_unregister(self._ptr)
+            self._registered = False
+        self.array = None
+        if getattr(self, "_shm", None) is not None:
+            self._shm.close()
+            if self.owner:
+                try:
+                    self._shm.unlink()
+                except FileNotFoundError:  # pragma: no cover
+                    pass
+            self._shm = None
+        if getattr(self, "_file", None) is not None:
+            self._map.close()
+            os.close(self._file[0])
+            if self.owner:
+                try:
+                    os.unlink(self._file[1])
+                except FileNotFoundError:  # pragma: no cover
+                    pass
+            self._file = None
 
     def __del__(self):
         try:
@@ -281,6 +375,72 @@ class KernelJob:
         if self.placement == "p2p":
             return self._run_p2p(p_train, p_test, train_angles.device)
         return self._run_gather(p_train, p_test, train_angles.device)
+
+    # ---- host buffers in and out ----------------------------------------------------------
+    def host_outputs(self) -> tuple:
+        """(K_train, K_cross) host matrices for :meth:`run_host`: shared-memory segments that
+        rank 0 creates and every rank maps (collective call).  Rank 0 reads the results from
+        their ``array`` views."""
+        lay = self.layout
+        if self.world == 1:
+            return (SharedHostMatrix(lay.n_train, lay.n_train),
+                    SharedHostMatrix(lay.n_test, lay.n_train) if lay.n_test else None)
+        names = None
+        if self.rank == 0:
+            mats = [SharedHostMatrix(lay.n_train, lay.n_train),
+                    SharedHostMatrix(lay.n_test, lay.n_train) if lay.n_test else None]
+            names = [m.name if m is not None else None for m in mats]
+        box = [names]
+        dist.broadcast_object_list(box, src=0, group=self.group)
+        if self.rank != 0:
+            mats = [SharedHostMatrix(lay.n_train, lay.n_train, name=box[0][0]),
+                    SharedHostMatrix(lay.n_test, lay.n_train, name=box[0][1])
+                    if lay.n_test else None]
+        dist.barrier(group=self.group)
+        return tuple(mats)
+
+    def run_host(self, train_host, test_host, out_train: SharedHostMatrix,
+                 out_test: SharedHostMatrix | None = None) -> None:
+        """Host angles in (pinned numpy arrays avoid a staging copy), host matrices out: the
+        job runs as :meth:`run` (p2p placement: every rank's sweep stores into rank 0's
+        matrices), then each rank copies rows [r N / W, (r + 1) N / W) of both matrices from
+        rank 0's GPU into the shared host matrices over its own PCIe link."""
+        lay = self.layout
+        dev_ = torch.device("cuda", torch.cuda.current_device())
+        tr = torch.from_numpy(np.ascontiguousarray(train_host)).to(dev_, non_blocking=True)
+        te = (torch.from_numpy(np.ascontiguousarray(test_host)).to(dev_, non_blocking=True)
+              if lay.n_test else None)
+        K, Kx = self.run(tr, te)
+        if self.world > 1 and self.placement != "p2p":
+            # gather placement: the matrices exist on rank 0 only
+            if self.rank == 0:
+                self._drain(K.data_ptr(), out_train, 0, lay.n_train)
+                if lay.n_test:
+                    self._drain(Kx.data_ptr(), out_test, 0, lay.n_test)
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)
+            return
+        if self.world == 1:
+            srcs = (K.data_ptr(), Kx.data_ptr() if lay.n_test else 0)
+        else:
+            srcs = (self._shared[0].ptr, self._shared[1].ptr if lay.n_test else 0)
+        for src, out, rows in ((srcs[0], out_train, lay.n_train),
+                               (srcs[1], out_test, lay.n_test)):
+            if rows:
+                lo, hi = shard_range(rows, self.rank, self.world)
+                self._drain(src, out, lo, hi)
+        torch.cuda.current_stream().synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    @staticmethod
+    def _drain(src_ptr: int, out: SharedHostMatrix, lo: int, hi: int) -> None:
+        if hi <= lo:
+            return
+        row = out.cols * 8
+        _native.check(_native.lib().qk_copy_d2h(out.array.ctypes.data + lo * row,
+                                                src_ptr + lo * row, (hi - lo) * row,
+                                                torch.cuda.current_stream().cuda_stream))
 
     def close(self) -> None:
         if self._shared:

@@ -43,11 +43,22 @@ def worker(rank, world, port, placement, layers, q):
         for _ in range(2):  # the second run reuses the shared matrices / buffers
             K, Kx = job.run(torch.as_tensor(Xtr, device="cuda"),
                             torch.as_tensor(Xte, device="cuda"))
+        # host buffers in and out: every rank drains its row slice into shared host memory
+        out_K, out_Kx = job.host_outputs()
+        out_K.array[:] = -1.0
+        out_Kx.array[:] = -1.0
+        dist.barrier()
+        job.run_host(Xtr, Xte, out_K, out_Kx)
         if rank == 0:
             cfg = FeatureMapConfig(WIDTH, layers=layers)
-            ok = (np.array_equal(K.cpu().numpy(), compute_kernel_matrix(Xtr, cfg).entries),
-                  np.array_equal(Kx.cpu().numpy(), compute_cross_kernel(Xte, Xtr, cfg).entries))
+            Kr = compute_kernel_matrix(Xtr, cfg).entries
+            Kxr = compute_cross_kernel(Xte, Xtr, cfg).entries
+            ok = (np.array_equal(K.cpu().numpy(), Kr) and np.array_equal(out_K.array, Kr),
+                  np.array_equal(Kx.cpu().numpy(), Kxr) and np.array_equal(out_Kx.array, Kxr))
             q.put(ok)
+        dist.barrier()
+        out_K.close()
+        out_Kx.close()
         dist.barrier()
         job.close()
         dist.destroy_process_group()
