@@ -180,6 +180,11 @@ qk_status qk_ipc_close(void* d_ptr);
 qk_status qk_host_register(void* h_ptr, size_t bytes);
 qk_status qk_host_unregister(void* h_ptr);
 qk_status qk_copy_d2h(void* h_dst, const void* d_src, size_t bytes, void* stream);
+/* The input side likewise: each rank uploads its slice of the angles into rank 0's shared
+ * angle buffer (qk_copy_h2d to a peer address) and then pulls the whole set over NVLink
+ * (qk_copy_d2d from the peer address). */
+qk_status qk_copy_h2d(void* d_dst, const void* h_src, size_t bytes, void* stream);
+qk_status qk_copy_d2d(void* d_dst, const void* d_src, size_t bytes, void* stream);
 
 /* ---- dense state-vector ground truth (checker beyond the reference's 24-qubit guard) ----
  * Replaces the reference's brute-force simulator (statevector.py:41-70, simulate /

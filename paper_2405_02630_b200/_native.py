@@ -75,6 +75,8 @@ _SIGNATURES = {
     "qk_host_register": (ctypes.c_int, [_c_vp, _c_sz]),
     "qk_host_unregister": (ctypes.c_int, [_c_vp]),
     "qk_copy_d2h": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
+    "qk_copy_h2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
+    "qk_copy_d2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
     "qk_statevector_bytes": (_c_sz, [ctypes.c_int32]),
     "qk_statevector_amplitude": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _c_vp, _c_vp,
                                                 _c_vp, ctypes.POINTER(ctypes.c_double), _c_vp]),

@@ -941,6 +941,22 @@ qk_status qk_host_unregister(void* h_ptr) {
   return cuda_err(cudaHostUnregister(h_ptr), "cudaHostUnregister");
 }
 
+qk_status qk_copy_h2d(void* d_dst, const void* h_src, size_t bytes, void* stream) {
+  if (bytes == 0) return QK_OK;
+  if (d_dst == nullptr || h_src == nullptr) return set_error(QK_ERR_VALUE, "NULL pointer");
+  return cuda_err(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice,
+                                  static_cast<cudaStream_t>(stream)),
+                  "H2D copy");
+}
+
+qk_status qk_copy_d2d(void* d_dst, const void* d_src, size_t bytes, void* stream) {
+  if (bytes == 0) return QK_OK;
+  if (d_dst == nullptr || d_src == nullptr) return set_error(QK_ERR_VALUE, "NULL pointer");
+  return cuda_err(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDeviceToDevice,
+                                  static_cast<cudaStream_t>(stream)),
+                  "D2D copy");
+}
+
 qk_status qk_copy_d2h(void* h_dst, const void* d_src, size_t bytes, void* stream) {
   if (bytes == 0) return QK_OK;
   if (h_dst == nullptr || d_src == nullptr) return set_error(QK_ERR_VALUE, "NULL pointer");

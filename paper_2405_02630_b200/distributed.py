@@ -407,9 +407,15 @@ class KernelJob:
         rank 0's GPU into the shared host matrices over its own PCIe link."""
         lay = self.layout
         dev_ = torch.device("cuda", torch.cuda.current_device())
-        tr = torch.from_numpy(np.ascontiguousarray(train_host)).to(dev_, non_blocking=True)
-        te = (torch.from_numpy(np.ascontiguousarray(test_host)).to(dev_, non_blocking=True)
-              if lay.n_test else None)
+        Xtr = np.ascontiguousarray(train_host, dtype=np.float64)
+        Xte = np.ascontiguousarray(test_host, dtype=np.float64) if lay.n_test else None
+        if self.world > 1 and self.placement == "p2p" and self._shared is None:
+            self._setup_shared()  # collective; falls back to the gather placement if needed
+        if self.world == 1 or self.placement != "p2p":
+            tr = torch.from_numpy(Xtr).to(dev_, non_blocking=True)
+            te = torch.from_numpy(Xte).to(dev_, non_blocking=True) if lay.n_test else None
+        else:
+            tr, te = self._upload_split(Xtr, Xte, dev_)
         K, Kx = self.run(tr, te)
         if self.world > 1 and self.placement != "p2p":
             # gather placement: the matrices exist on rank 0 only
@@ -433,6 +439,40 @@ class KernelJob:
         if self.world > 1:
             dist.barrier(group=self.group)
 
+    def _upload_split(self, Xtr: np.ndarray, Xte, dev_):
+        """Each rank uploads its row slice of the angles into rank 0's shared angle buffer
+        (its own PCIe link), then every rank pulls the whole set from rank 0 over NVLink."""
+        lay = self.layout
+        width = Xtr.shape[1]
+        rows = lay.n_train + lay.n_test
+        if getattr(self, "_angles", None) is None:
+            if self.rank == 0:
+                mat = SharedMatrix(rows, width)
+                handle = mat.export()
+            else:
+                mat, handle = None, None
+            box = [handle]
+            dist.broadcast_object_list(box, src=0, group=self.group)
+            if self.rank != 0:
+                mat = SharedMatrix(rows, width, handle=box[0])
+            self._angles = mat
+            self._angles_local = torch.empty((rows, width), dtype=torch.float64, device=dev_)
+        mat, local = self._angles, self._angles_local
+        lib = _native.lib()
+        stream = torch.cuda.current_stream().cuda_stream
+        row = width * 8
+        for X, base, n in ((Xtr, 0, lay.n_train), (Xte, lay.n_train, lay.n_test)):
+            if n:
+                lo, hi = shard_range(n, self.rank, self.world)
+                if hi > lo:
+                    _native.check(lib.qk_copy_h2d(mat.ptr + (base + lo) * row,
+                                                  X.ctypes.data + lo * row, (hi - lo) * row,
+                                                  stream))
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+        _native.check(lib.qk_copy_d2d(local.data_ptr(), mat.ptr, rows * row, stream))
+        return local[:lay.n_train], (local[lay.n_train:] if lay.n_test else None)
+
     @staticmethod
     def _drain(src_ptr: int, out: SharedHostMatrix, lo: int, hi: int) -> None:
         if hi <= lo:
@@ -447,3 +487,6 @@ class KernelJob:
             for m in self._shared:
                 m.close()
             self._shared = None
+        if getattr(self, "_angles", None) is not None:
+            self._angles.close()
+            self._angles = None
