@@ -403,6 +403,17 @@ StreamWriteValue32Fn stream_write_value32() {
 // kArriveBlocks plane blocks on w->h2d_stream, each followed by an arrival mark, and the
 // sweep starts at once — its CTAs build each plane block as soon as its chunk has landed, so
 // the H2D of the inputs overlaps the sweep instead of preceding it.
+// Under a tool that serialises GPU work (ncu, compute-sanitizer: CUDA_INJECTION64_PATH is
+// set) the sweep could not see chunks land while it runs; there the chunks are copied first
+// (QK_FUSED_PREARRIVE=1 forces this), so the in-kernel build never waits.
+bool fused_prearrive() {
+  static const bool on = [] {
+    const char* v = getenv("QK_FUSED_PREARRIVE");
+    return getenv("CUDA_INJECTION64_PATH") != nullptr || (v != nullptr && v[0] == '1');
+  }();
+  return on;
+}
+
 bool fused_build_enabled(const Plan& p) {
   static const bool on = [] {
     const char* v = getenv("QK_FUSED_BUILD");
@@ -556,11 +567,21 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   cudaEventCreateWithFlags(&reset, cudaEventDisableTiming);
   cudaEventRecord(reset, w->stream);
   if (trace) trace->mark(2, w->stream);
+  if (after_launch && fused_prearrive()) {  // feed the chunks first (serialising tools)
+    if (qk_status s = after_launch()) {
+      cudaEventDestroy(reset);
+      return s;
+    }
+    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) {
+      cudaEventDestroy(reset);
+      return cuda_err(e, "H2D chunks");
+    }
+  }
   if (qk_status s = launch()) {
     cudaEventDestroy(reset);
     return s;
   }
-  if (after_launch) {
+  if (after_launch && !fused_prearrive()) {
     cudaStreamQuery(w->stream);  // the sweep is on its way; feed it
     if (qk_status s = after_launch()) {
       cudaStreamSynchronize(w->stream);  // a sweep waiting for missing chunks traps (20 s)

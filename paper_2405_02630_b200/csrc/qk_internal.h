@@ -64,11 +64,12 @@ int64_t blocks_for(int64_t n_samples);
 // touches it and whole warps of those tiles can skip it.
 QK_HD inline int sample_pad(int64_t n) { return int((kTile - n % kTile) % kTile); }
 
-// Progress-counter increments per finished tile (host pipelines): L <= 2 one per tile, L = 3, 4
+// Progress-counter increments per finished tile (host pipelines): L <= 2 two per tile (a tile
+// of the last wave may run as two row halves, one each), L = 3, 4
 // one per 16x16 sub-tile, L >= 5 one per pair group of the deep sweep (16, 8, 4, 1 pairs at
 // L = 5, 6, 7, 8: Deep<M>::PP in qk_sweep.cu).
 QK_HD constexpr uint32_t progress_unit(int layers) {
-  if (layers <= 2) return 1u;
+  if (layers <= 2) return 2u;
   if (layers <= 4) return 16u;
   const int pp = layers == 5 ? 16 : layers == 6 ? 8 : layers == 7 ? 4 : 1;
   return uint32_t(kTile * kTile / pp);

@@ -522,6 +522,7 @@ struct SweepArgs {
   PlaneSrc src[2];
   unsigned long long* stats;  // diagnostics (QK_FUSED_STATS=1): per CTA ns in ensure, t0, t_end
   unsigned long long* next_tile;  // dynamic tile claims beyond the first wave (zeroed per launch)
+  int64_t n_split;  // the last n_split tiles run as two row halves each (finer last wave)
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -615,8 +616,74 @@ struct TileXY {
   int prob;
 };
 
+// A CTA's claimed work item (dynamic tile schedule; see sweep_kernel).
+struct Claim {
+  int64_t g;  // launch-local work item (>= n_items: none)
+  int64_t t;  // launch-local tile index
+  int bi, bj, prob;
+  int half;   // -1: whole tile; 0 / 1: tile rows 0-31 / 32-63 only
+};
+
+// Shared-memory state of the fused plane build of one CTA.
+struct FusedState {
+  int ensured;      // CTA-local tile number up to which the planes are known to exist
+  int set_done[2];  // this CTA has seen every block of plane set s built (and fenced)
+  int build_flag;
+  unsigned long long stat[5];  // QK_FUSED_STATS: ensure ns, t0, first tile, build ns, builds
+};
+
+// Fused plane build, CTA-wide, out of line (keeps the sweep's registers for the sweep): make
+// the plane blocks of this CTA's tiles (ensured, last] exist, waiting for them; with
+// `lookahead` also build (never wait for) those of tile last + 1.  Once this CTA has seen
+// every block of a set built (one acquire of the set's counter, then one proxy fence), tiles
+// of that set need no check, barrier or fence.  `a` is a local copy of the kernel arguments.
+__device__ __noinline__ void fused_ensure(const SweepArgs* a, const Claim* ring, int64_t n_items,
+                                          int64_t last, bool lookahead, FusedState* fs,
+                                          double* stage_T) {
+  auto valid = [&](int64_t k) { return ring[k & 7].g < n_items; };
+  while (last > fs->ensured && !valid(last)) --last;  // claims past the end of the list
+  bool need = false;
+  for (int64_t k = fs->ensured + 1; k <= last; ++k) {
+    const Claim& c = ring[k & 7];
+    need |= !fs->set_done[c.prob ? a->set_rows2 : a->set_rows] || !fs->set_done[a->set_cols];
+  }
+  if (!need) {
+    // every thread computed the same `last` and stores the same value: a thread that reads
+    // the new value scans an empty range and reaches the same (no-op) outcome
+    if (last > fs->ensured) fs->ensured = int(last);
+    return;
+  }
+  __syncthreads();  // every warp is past the previous epilogue (stage_T is the build tile)
+  const unsigned long long e0 = a->stats ? global_ns() : 0;
+  unsigned long long* bst = a->stats ? fs->stat + 3 : nullptr;
+  double (*tile)[65] = reinterpret_cast<double (*)[65]>(stage_T);
+  auto blocks = [&](const Claim& c, bool wait) {
+    const int si = c.prob ? a->set_rows2 : a->set_rows;
+    if (!fs->set_done[si])
+      ensure_block(a->src[si], c.bi, a->n_pad, a->front, a->width, a->half, tile,
+                   &fs->build_flag, wait, bst);
+    if (!fs->set_done[a->set_cols])
+      ensure_block(a->src[a->set_cols], c.bj, a->n_pad, a->front, a->width, a->half, tile,
+                   &fs->build_flag, wait, bst);
+  };
+  for (int64_t k = fs->ensured + 1; k <= last; ++k) blocks(ring[k & 7], true);
+  if (lookahead && valid(last + 1)) blocks(ring[(last + 1) & 7], false);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fs->ensured = int(last);
+    for (int s = 0; s < 2; ++s)
+      if (!fs->set_done[s] && ld_acquire_gpu(a->src[s].built) == a->src[s].nblocks)
+        fs->set_done[s] = 1;
+    if (a->stats) fs->stat[0] += global_ns() - e0;
+  }
+  // the planes were written through the generic proxy; the bulk copies read them through
+  // the async proxy
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncthreads();  // ensured, set_done
+}
+
 template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
-__global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
+__device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   using St = typename BondT<LAYERS>::type;
   constexpr int kRI = Geo<RI>::kRI, kWarps = Geo<RI>::kWarps;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -635,20 +702,26 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   // (thread 0) at the start of tile k and published by a CTA barrier.  Claims live in a small
   // shared ring indexed by the CTA-local tile number.
   const int kLook = 1 + (kStages - 1) / nchunks;
-  struct Claim {
-    int64_t g;  // launch-local tile index (>= n_tiles: none)
-    int bi, bj, prob;
-  };
   __shared__ Claim ring[8];
   int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
   double* stage_T = reinterpret_cast<double*>(table + kTileTable);  // epilogue staging tile
+  // Work items: tiles [0, n_tiles - n_split) whole, then the last n_split tiles as two row
+  // halves each, so the final wave ends in half-tile steps (a half tile takes about half the
+  // time: the warps of the other half skip the sweep like padding rows do).
+  const int64_t n_whole = a.n_tiles - a.n_split, n_items = a.n_tiles + a.n_split;
   auto claim = [&](int64_t k) {  // thread 0 only
     Claim c;
     c.g = k == 0 ? int64_t(blockIdx.x)
                  : int64_t(gridDim.x) + int64_t(atomicAdd(a.next_tile, 1ull));
     c.bi = c.bj = c.prob = 0;
-    if (c.g < a.n_tiles) {
-      const int64_t g = a.tile_begin + c.g;
+    c.half = -1;
+    c.t = c.g;
+    if (c.g >= n_whole && c.g < n_items) {
+      c.t = n_whole + (c.g - n_whole) / 2;
+      c.half = int((c.g - n_whole) % 2);
+    }
+    if (c.g < n_items) {
+      const int64_t g = a.tile_begin + c.t;
       int64_t bi, bj;
       if (MODE == kModeGram || (MODE == kModeJob && g < a.n_first)) {
         decode_upper(g, a.nb_rows, bi, bj);
@@ -663,7 +736,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     }
     ring[k & 7] = c;
   };
-  auto valid = [&](int64_t k) { return ring[k & 7].g < a.n_tiles; };
+  auto valid = [&](int64_t k) { return ring[k & 7].g < n_items; };
   auto tile_of = [&](int64_t k) -> TileXY {
     const Claim& c = ring[k & 7];
     return TileXY{c.bi, c.bj, c.prob};
@@ -671,66 +744,16 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
   if (tid == 0)
     for (int64_t k = 0; k <= kLook; ++k) claim(k);
   __syncthreads();
-  // fused plane build: tiles whose chunks may be issued before the next ensure point.  Once
-  // this CTA has seen every block of a set built (one acquire of the set's counter, then one
-  // proxy fence), tiles of that set need no check, barrier or fence.
-  __shared__ int build_flag;
-  __shared__ int set_done[2];
-  if (FUSED && tid == 0) set_done[0] = set_done[1] = 0;
-  if (FUSED) __syncthreads();
-  int64_t ensured = -1;
-  unsigned long long st_ns = 0, st_t0 = FUSED && a.stats ? global_ns() : 0, st_first = 0;
-  __shared__ unsigned long long bstat_s[2];
-  unsigned long long* bstat = nullptr;
-  if (FUSED && a.stats) {
-    if (tid == 0) bstat_s[0] = bstat_s[1] = 0;
-    bstat = bstat_s;
+  // fused plane build state (shared memory) and a local copy of the arguments for it
+  __shared__ FusedState fs;
+  if (FUSED && tid == 0) {
+    fs.ensured = -1;
+    fs.set_done[0] = fs.set_done[1] = 0;
+    for (int q = 0; q < 5; ++q) fs.stat[q] = 0;
+    if (a.stats) fs.stat[1] = global_ns();
   }
-  auto ensure_upto = [&](int64_t last, bool lookahead) {
-    while (last > ensured && !valid(last)) --last;  // claims past the end of the list
-    bool need = false;
-    for (int64_t k = ensured + 1; k <= last; ++k) {
-      const TileXY t = tile_of(k);
-      need |= !set_done[t.prob ? a.set_rows2 : a.set_rows] || !set_done[a.set_cols];
-    }
-    if (!need) {
-      ensured = last > ensured ? last : ensured;
-      return;
-    }
-    __syncthreads();  // every warp is past the previous epilogue (stage_T is the build tile)
-    const unsigned long long e0 = a.stats ? global_ns() : 0;
-    double (*tile)[65] = reinterpret_cast<double (*)[65]>(stage_T);
-    for (; ensured < last;) {
-      const TileXY t = tile_of(++ensured);
-      const int si = t.prob ? a.set_rows2 : a.set_rows;
-      if (!set_done[si])
-        ensure_block(si ? a.src[1] : a.src[0], t.bi, a.n_pad, a.front, a.width, a.half, tile,
-                     &build_flag, true, bstat);
-      if (!set_done[a.set_cols])
-        ensure_block(a.set_cols ? a.src[1] : a.src[0], t.bj, a.n_pad, a.front, a.width, a.half,
-                     tile, &build_flag, true, bstat);
-    }
-    if (lookahead && valid(last + 1)) {  // build (never wait for) the next tile's blocks
-      const TileXY t = tile_of(last + 1);
-      const int si = t.prob ? a.set_rows2 : a.set_rows;
-      if (!set_done[si])
-        ensure_block(si ? a.src[1] : a.src[0], t.bi, a.n_pad, a.front, a.width, a.half, tile,
-                     &build_flag, false, bstat);
-      if (!set_done[a.set_cols])
-        ensure_block(a.set_cols ? a.src[1] : a.src[0], t.bj, a.n_pad, a.front, a.width, a.half,
-                     tile, &build_flag, false, bstat);
-    }
-    if (tid == 0) {
-      if (!set_done[0] && ld_acquire_gpu(a.src[0].built) == a.src[0].nblocks) set_done[0] = 1;
-      if (!set_done[1] && ld_acquire_gpu(a.src[1].built) == a.src[1].nblocks) set_done[1] = 1;
-    }
-    // the planes were written through the generic proxy; the bulk copies read them through
-    // the async proxy
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncthreads();  // set_done
-    if (a.stats) st_ns += global_ns() - e0;
-  };
-  if constexpr (FUSED) ensure_upto((kStages - 1) / nchunks, false);
+  if (FUSED) __syncthreads();
+  if constexpr (FUSED) fused_ensure(&a, ring, n_items, (kStages - 1) / nchunks, false, &fs, stage_T);
   auto issue = [&](int64_t f) {  // fill stage f % kStages with item f (if its tile exists)
     const int64_t k = f / nchunks;
     if (!valid(k)) return;
@@ -771,14 +794,17 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     // fused build: the blocks of tile k + 1 are needed once its first chunks are issued
     // (during tile k); ensure them here, where no bond state is live
     if constexpr (FUSED) {
-      ensure_upto(k + 1 + (kStages - 1) / nchunks, true);
-      if (k == 0 && a.stats) st_first = global_ns();
+      fused_ensure(&a, ring, n_items, k + 1 + (kStages - 1) / nchunks, true, &fs, stage_T);
+      if (k == 0 && a.stats && tid == 0) fs.stat[2] = global_ns();
     }
     const TileXY tk = tile_of(k);
     // padding rows of this tile (front of plane block 0): warps made only of them skip the
     // sweep (they still release every stage) — the ragged sample block costs ~1/4 of a tile
     const int pad_r = tk.bi == 0 ? (tk.prob ? a.pad_rows2 : a.pad_rows) : 0;
-    const bool idle = warp_row_end <= pad_r;
+    const int half = ring[k & 7].half;
+    const int r_lo = half == 1 ? kTile / 2 : 0, r_hi = half == 0 ? kTile / 2 : kTile;
+    const bool idle = warp_row_end <= (pad_r > r_lo ? pad_r : r_lo) ||
+                      warp_row_end - (32 / kTX) * kRI >= r_hi;
 #pragma unroll
     for (int r = 0; r < kRI; ++r)
 #pragma unroll
@@ -834,13 +860,14 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
     const int64_t bi = t.bi, bj = t.bj;
     const bool gram = MODE == kModeGram || (MODE == kModeJob && t.prob == 0);
     if (OUT == QK_OUT_PACKED) {
-      double* o = a.out + ring[k & 7].g * int64_t(kTile * kTile);
+      double* o = a.out + ring[k & 7].t * int64_t(kTile * kTile);
 #pragma unroll
       for (int r = 0; r < kRI; ++r)
 #pragma unroll
         for (int c = 0; c < kRJ; ++c)
-          o[(ty * kRI + r) * kTile + tx + kTX * c] =
-              kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
+          if (ty * kRI + r >= r_lo && ty * kRI + r < r_hi)
+            o[(ty * kRI + r) * kTile + tx + kTX * c] =
+                kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
     } else if (QK_EPI == 1) {
       // Per-warp epilogue, no CTA barrier: the warp's 2*kRI rows go out straight from the
       // registers (each store instruction writes two 128 B row segments), and the Gram mirror
@@ -907,7 +934,7 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       const int64_t n_rows = t.prob ? a.n_rows2 : a.n_rows;
       const int64_t i0 = bi * kTile - (t.prob ? a.pad_rows2 : a.pad_rows);
       const int64_t j0 = bj * kTile - (gram ? a.pad_rows : a.pad_cols);
-      for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+      for (int e = r_lo * kTile + tid; e < r_hi * kTile; e += blockDim.x) {
         const int il = e / kTile, jl = e % kTile;  // consecutive threads: consecutive columns
         const int64_t i = i0 + il, j = j0 + jl;
         if (gram) {
@@ -918,8 +945,9 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
         }
       }
       if (gram) {
-        for (int e = tid; e < kTile * kTile; e += blockDim.x) {
-          const int jl = e / kTile, il = e % kTile;  // mirror: row j of K, consecutive i
+        const int span = r_hi - r_lo;
+        for (int e = tid; e < kTile * span; e += blockDim.x) {
+          const int jl = e / span, il = r_lo + e % span;  // mirror: row j of K, consecutive i
           const int64_t i = i0 + il, j = j0 + jl;
           if (i >= 0 && i < j && j < n_rows) out[j * ld + i] = stage_T[il * (kTile + 1) + jl];
         }
@@ -930,19 +958,35 @@ __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const Sweep
       // publish the finished tile to a copy stream waiting on its super-row counter
       QK_PROGRESS_FENCE();
       __syncthreads();
-      if (tid == 0) atomicAdd(prog + bi, 1u);  // per tile row
+      if (tid == 0) atomicAdd(prog + bi, half < 0 ? 2u : 1u);  // per tile row: 2 per tile
     }
   }
   if constexpr (FUSED) {
     if (a.stats != nullptr && tid == 0) {
-      a.stats[6 * blockIdx.x] = st_ns;
-      a.stats[6 * blockIdx.x + 1] = st_t0;
+      a.stats[6 * blockIdx.x] = fs.stat[0];
+      a.stats[6 * blockIdx.x + 1] = fs.stat[1];
       a.stats[6 * blockIdx.x + 2] = global_ns();
-      a.stats[6 * blockIdx.x + 3] = bstat_s[0];
-      a.stats[6 * blockIdx.x + 4] = bstat_s[1];
-      a.stats[6 * blockIdx.x + 5] = st_first;
+      a.stats[6 * blockIdx.x + 3] = fs.stat[3];
+      a.stats[6 * blockIdx.x + 4] = fs.stat[4];
+      a.stats[6 * blockIdx.x + 5] = fs.stat[2];
     }
   }
+}
+
+template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
+__global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
+  sweep_body<LAYERS, MODE, OUT, RI, false>(a);
+}
+
+// The in-kernel plane build adds an out-of-line call per tile; capping the registers at the
+// plain kernel's count keeps ptxas from re-allocating the sweep loop around it.
+#ifndef QK_FUSED_MAXNREG
+#define QK_FUSED_MAXNREG 120
+#endif
+template <int LAYERS, int MODE, int OUT, int RI>
+__global__ void __maxnreg__(QK_FUSED_MAXNREG)
+    sweep_kernel_fused(const SweepArgs a) {
+  sweep_body<LAYERS, MODE, OUT, RI, true>(a);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1342,7 +1386,8 @@ static qk_status tile_counter(cudaStream_t st, unsigned long long** out) {
 template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
 static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
   if (qk_status s = tile_counter(st, &a.next_tile)) return s;
-  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI, FUSED>;
+  auto kern = FUSED ? sweep_kernel_fused<LAYERS, MODE, OUT, RI>
+                    : sweep_kernel<LAYERS, MODE, OUT, RI, false>;
   constexpr int threads = Geo<RI>::kThreads;
   // per call: the attribute is per device and costs microseconds
   cudaError_t e =
@@ -1355,7 +1400,14 @@ static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
   const int sms = sm_count();
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
   int64_t grid = int64_t(sms) * per_sm;
-  if (grid > a.n_tiles) grid = a.n_tiles;
+  // the last wave runs as half tiles (QK_EPI == 1 epilogue: whole tiles only)
+  static const int split_mode = [] {  // QK_HALF_TILES: 0 off, 1 on, 2 plain kernel only
+    const char* v = getenv("QK_HALF_TILES");
+    return v == nullptr ? 1 : v[0] - '0';
+  }();
+  const bool split = QK_EPI != 1 && (split_mode == 1 || (split_mode == 2 && !FUSED));
+  a.n_split = split ? std::min<int64_t>(a.n_tiles, grid) : 0;
+  if (grid > a.n_tiles + a.n_split) grid = a.n_tiles + a.n_split;
   kern<<<unsigned(grid), threads, kSmemBytes, st>>>(a);
   return cuda_status(cudaGetLastError(), "sweep launch");
 }
