@@ -403,13 +403,26 @@ StreamWriteValue32Fn stream_write_value32() {
 // kArriveBlocks plane blocks on w->h2d_stream, each followed by an arrival mark, and the
 // sweep starts at once — its CTAs build each plane block as soon as its chunk has landed, so
 // the H2D of the inputs overlaps the sweep instead of preceding it.
-// Under a tool that serialises GPU work (ncu, compute-sanitizer: CUDA_INJECTION64_PATH is
-// set) the sweep could not see chunks land while it runs; there the chunks are copied first
-// (QK_FUSED_PREARRIVE=1 forces this), so the in-kernel build never waits.
+// Under a tool that serialises GPU work (ncu, compute-sanitizer) the sweep could not see
+// chunks land while it runs; there the chunks are copied first (QK_FUSED_PREARRIVE=1 forces
+// this), so the in-kernel build never waits.  The tools are recognised by their injection
+// environment or by their injection library in the process's mappings.
 bool fused_prearrive() {
   static const bool on = [] {
     const char* v = getenv("QK_FUSED_PREARRIVE");
-    return getenv("CUDA_INJECTION64_PATH") != nullptr || (v != nullptr && v[0] == '1');
+    if (v != nullptr) return v[0] == '1';
+    for (const char* e : {"CUDA_INJECTION64_PATH", "NVIDIA_PROCESS_INJECTION_XML_TARGET_SETTINGS",
+                          "NV_COMPUTE_PROFILER_PERFWORKS_DIR"})
+      if (getenv(e) != nullptr) return true;
+    FILE* f = fopen("/proc/self/maps", "r");
+    if (f == nullptr) return false;
+    char line[1024];
+    bool hit = false;
+    while (!hit && fgets(line, sizeof line, f) != nullptr)
+      hit = strstr(line, "TreeLauncherTargetInjection") != nullptr ||
+            strstr(line, "libsanitizer-collection") != nullptr;
+    fclose(f);
+    return hit;
   }();
   return on;
 }
