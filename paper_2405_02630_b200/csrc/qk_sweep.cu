@@ -1412,25 +1412,28 @@ static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
   return cuda_status(cudaGetLastError(), "sweep launch");
 }
 
-// Micro-tile rows per thread: 2 (512 threads, 126 registers, 16 warps/SM; measured best) or
-// 4 (256 threads, 4x4 micro-tiles); QK_SWEEP_RI=4 selects the latter (tuning knob).
-static int sweep_ri() {
-  static int ri = [] {
+// Micro-tile rows per thread: 2 (512 threads, 2x4 micro-tiles, 16 warps/SM) or 4 (256
+// threads, 4x4 micro-tiles).  Measured (784 qubits, one B200): L = 2 RI 2 1.206 vs RI 4
+// 1.171 G entries/s; L = 1 (3 FP64 instructions per pair-qubit, so the shared-memory loads
+// per pair matter) RI 2 4.18 vs RI 4 5.49 G entries/s.  QK_SWEEP_RI=2/4 overrides.
+static int sweep_ri(int layers) {
+  static int forced = [] {
     const char* v = getenv("QK_SWEEP_RI");
-    return (v != nullptr && v[0] == '4') ? 4 : 2;
+    return v == nullptr ? 0 : (v[0] == '4' ? 4 : 2);
   }();
-  return ri;
+  if (forced) return forced;
+  return layers == 1 ? 4 : 2;
 }
 
 template <int LAYERS, int MODE, int OUT>
 static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   if constexpr (OUT == QK_OUT_DENSE) {  // the in-kernel plane build serves the host pipelines
     if (a.fused) {
-      if (sweep_ri() == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, true>(a, st);
+      if (sweep_ri(LAYERS) == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, true>(a, st);
       return launch_sweep_ri<LAYERS, MODE, OUT, 4, true>(a, st);
     }
   }
-  if (sweep_ri() == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, false>(a, st);
+  if (sweep_ri(LAYERS) == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, false>(a, st);
   return launch_sweep_ri<LAYERS, MODE, OUT, 4, false>(a, st);
 }
 
