@@ -702,6 +702,9 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   // (thread 0) at the start of tile k and published by a CTA barrier.  Claims live in a small
   // shared ring indexed by the CTA-local tile number.
   const int kLook = 1 + (kStages - 1) / nchunks;
+  // the fused plane build also looks one tile further ahead (it builds, never waits for, the
+  // blocks of tile k + kLook + 1), so that tile is claimed too
+  const int kClaim = kLook + (FUSED ? 1 : 0);
   __shared__ Claim ring[8];
   int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
   double* stage_T = reinterpret_cast<double*>(table + kTileTable);  // epilogue staging tile
@@ -742,7 +745,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
     return TileXY{c.bi, c.bj, c.prob};
   };
   if (tid == 0)
-    for (int64_t k = 0; k <= kLook; ++k) claim(k);
+    for (int64_t k = 0; k <= kClaim; ++k) claim(k);
   __syncthreads();
   // fused plane build state (shared memory) and a local copy of the arguments for it
   __shared__ FusedState fs;
@@ -787,8 +790,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   St st[kRI][kRJ];
   int64_t f = 0;
   for (int64_t k = 0; valid(k); ++k) {
-    if (k > 0) {  // claim tile k + kLook (its chunks are issued during tile k)
-      if (tid == 0) claim(k + kLook);
+    if (k > 0) {  // claim tile k + kClaim (the chunks of tile k + kLook are issued during tile k)
+      if (tid == 0) claim(k + kClaim);
       __syncthreads();
     }
     // fused build: the blocks of tile k + 1 are needed once its first chunks are issued

@@ -1,7 +1,9 @@
-"""In-kernel plane build of the host pipelines (pinned angle buffers): the H2D goes up in
+"""In-kernel plane build of the host pipelines (opt-in, pinned angle buffers): the H2D goes up in
 chunks of plane blocks on its own stream and the persistent sweep builds each plane block
 itself as soon as its angles have landed.  It must reproduce the gate-build path (pageable
 inputs: upload, gate-build kernel, sweep) bit for bit, for every shape of the chunking."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -11,6 +13,18 @@ from paper_2405_02630_b200 import (FeatureMapConfig, RebindError, compute_cross_
                                    compute_kernel_matrices, compute_kernel_matrix)
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _fused_build_on():
+    """The in-kernel plane build is opt-in (QK_FUSED_BUILD=1, read on every call)."""
+    old = os.environ.get("QK_FUSED_BUILD")
+    os.environ["QK_FUSED_BUILD"] = "1"
+    yield
+    if old is None:
+        del os.environ["QK_FUSED_BUILD"]
+    else:
+        os.environ["QK_FUSED_BUILD"] = old
 
 
 def _pinned(a: np.ndarray) -> np.ndarray:
