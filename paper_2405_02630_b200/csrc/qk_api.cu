@@ -505,6 +505,27 @@ qk_status fused_setup(Workspace* w, const Plan& p, FusedBuild& fb, int n_sets, d
   return QK_OK;
 }
 
+// Head-first overlap of the input upload (pinned inputs, L = 2, the default host pipeline;
+// QK_HEAD_SPLIT=0 turns it off): the angles of the first B plane blocks go up and are
+// gate-built, the sweep runs the B x B Gram head (decode_gram orders it first) while the rest
+// of the angles upload on the h2d stream, then the rest is gate-built and swept.  B is the
+// smallest multiple of kGroup whose head keeps the GPU busy for as long as the remaining
+// upload takes (estimates: ~0.6 us per tile per qubit on 148 SMs, ~50 GB/s of H2D).
+int64_t choose_head(const Plan& p, int64_t n_train, int64_t n_test) {
+  const char* v = getenv("QK_HEAD_SPLIT");
+  if ((v != nullptr && v[0] == '0') || p.layers != 2) return 0;
+  const int64_t nb = blocks_for(n_train), pad = sample_pad(n_train);
+  const double tile_ms = 6e-4 * p.width, bw_bytes_per_ms = 50e6;
+  for (int64_t B = kGroup; B + kGroup <= nb; B += kGroup) {
+    const int64_t s1 = std::min<int64_t>(n_train, B * kTile - pad);
+    const double rest_ms = double((n_train - s1) + n_test) * p.width * 8 / bw_bytes_per_ms;
+    const double head_ms = double(B * (B + 1) / 2) / 148.0 * tile_ms;
+    if (rest_ms < 0.05) return 0;  // nothing worth hiding
+    if (head_ms >= rest_ms) return B;
+  }
+  return 0;
+}
+
 // One row-major result matrix a sweep launch fills and the copy stream drains to the host.
 struct DrainTarget {
   double* d_K;
@@ -731,47 +752,10 @@ extern "C" {
 
 qk_status qk_kernel_matrix_host(const qk_plan* plan, const double* h_angles, int64_t n_samples,
                                 double* h_K) {
-  const Plan* p;
-  if (qk_status s = check_plan(plan, &p)) return s;
+  // the train Gram alone is the joint pipeline without a test set (same drain, same head-first
+  // upload overlap for pinned inputs)
   if (n_samples < 0) return set_error(QK_ERR_VALUE, "n_samples must be >= 0");
-  if (n_samples == 0) return QK_OK;
-  if (!h_angles || !h_K) return set_error(QK_ERR_VALUE, "NULL host buffer");
-  Workspace* w;
-  std::unique_lock<std::mutex> lock;
-  if (qk_status s = workspace_for_current(&w, lock)) return s;
-  const int64_t N = n_samples;
-  const size_t xb = size_t(N) * p->width * sizeof(double);
-  if (qk_status s = w->ensure(0, xb)) return s;
-  if (qk_status s = w->ensure(1, qk_planes_bytes(plan, N))) return s;
-  if (qk_status s = w->ensure(2, size_t(N) * size_t(N) * sizeof(double))) return s;
-  double* dX = static_cast<double*>(w->buf[0]);
-  cudaStream_t st = w->stream;
-  Trace trace(st);
-  void* planes = w->buf[1];
-  const bool fused = fused_build_enabled(*p) && is_pinned(h_angles);
-  FusedBuild fb;
-  if (fused) {
-    if (qk_status s = fused_setup(w, *p, fb, 1, &dX, &N, &planes)) return s;
-    trace.mark(1, st);
-  } else {
-    if (qk_status s = upload(w, dX, h_angles, xb)) return s;
-    trace.mark(1, st);
-    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, sizeof(uint64_t), st))
-      return cuda_err(e, "sentinel reset");
-    if (qk_status s = launch_gate_build(*p, dX, N, p->width, w->buf[1], w->bad, st)) return s;
-  }
-  DrainTarget tg[1] = {{static_cast<double*>(w->buf[2]), h_K, N, N, kModeGram, nullptr}};
-  if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
-        return launch_sweep(*p, kModeGram, planes, N, planes, N, 0,
-                            qk_gram_tile_count(plan, N), tg[0].d_K, N, QK_OUT_DENSE, w->stream,
-                            tg[0].d_prog, fused ? &fb : nullptr);
-      }, &trace, fused ? std::function<qk_status()>([&] { return fused_h2d(w, fb.set[0], h_angles); })
-                       : std::function<qk_status()>()))
-    return s;
-  if (fused)
-    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
-  static const char* const names[1] = {"train"};
-  return check_bad(w->bad, 1, names);
+  return qk_kernel_matrices_host(plan, h_angles, n_samples, nullptr, 0, h_K, nullptr);
 }
 
 qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_t n_rows,
@@ -870,30 +854,76 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
     void* ps[2] = {dPt, dPs};
     if (qk_status s = fused_setup(w, *p, fb, n_test > 0 ? 2 : 1, dXs2, ns, ps)) return s;
     trace.mark(1, st);
-  } else {
-    if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
-    if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
-    trace.mark(1, st);
-    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
-      return cuda_err(e, "sentinel reset");
-    if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
-    if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
-      return s;
   }
   DrainTarget tg[2] = {{dKt, h_K_train, n_train, n_train, kModeGram, nullptr},
                        {dKs, h_K_cross, n_test, n_train, kModeCross, nullptr}};
   const int64_t nt = qk_job_tile_count(plan, n_train, n_test);
-  if (qk_status s = run_and_drain(w, *p, tg, n_test > 0 ? 2 : 1, [&] {
-        return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
-                          tg[1].d_prog, fused ? &fb : nullptr);
-      }, &trace, fused ? std::function<qk_status()>([&]() -> qk_status {
-        if (qk_status s = fused_h2d(w, fb.set[0], h_train)) return s;
-        return n_test > 0 ? fused_h2d(w, fb.set[1], h_test) : QK_OK;
-      }) : std::function<qk_status()>()))
-    return s;
-  if (fused) print_fused_stats(148);
-  if (fused)
-    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
+  const int n_targets = n_test > 0 ? 2 : 1;
+  const int64_t B = !fused && is_pinned(h_train) && (n_test == 0 || is_pinned(h_test))
+                        ? choose_head(*p, n_train, n_test)
+                        : 0;
+  if (B > 0) {
+    // head: its angles, its planes, then the head sweep with the rest uploading beside it
+    const int64_t s1 = std::min<int64_t>(n_train, B * kTile - sample_pad(n_train));
+    const size_t row = size_t(p->width) * sizeof(double);
+    if (cudaError_t e = cudaMemcpyAsync(dXt, h_train, size_t(s1) * row, cudaMemcpyHostToDevice,
+                                        st))
+      return cuda_err(e, "H2D head");
+    trace.mark(1, st);
+    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+      return cuda_err(e, "sentinel reset");
+    if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st, 0, B))
+      return s;
+    const int64_t n_head = B * (B + 1) / 2;
+    if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&]() -> qk_status {
+          if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, 0, n_head, dKt, dKs, st,
+                                        tg[0].d_prog, tg[1].d_prog, nullptr, B))
+            return s2;
+          cudaError_t e = cudaMemcpyAsync(dXt + s1 * p->width, h_train + s1 * p->width,
+                                          size_t(n_train - s1) * row, cudaMemcpyHostToDevice,
+                                          w->h2d_stream);
+          if (e == cudaSuccess && n_test > 0)
+            e = cudaMemcpyAsync(dXs, h_test, xsb, cudaMemcpyHostToDevice, w->h2d_stream);
+          cudaEvent_t up;
+          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&up, cudaEventDisableTiming);
+          if (e == cudaSuccess) {
+            e = cudaEventRecord(up, w->h2d_stream);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(st, up, 0);
+            cudaEventDestroy(up);
+          }
+          if (e != cudaSuccess) return cuda_err(e, "H2D rest");
+          if (qk_status s2 = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st, B))
+            return s2;
+          if (qk_status s2 = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
+            return s2;
+          return launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, st,
+                            tg[0].d_prog, tg[1].d_prog, nullptr, B);
+        }, &trace))
+      return s;
+  } else {
+    if (!fused) {
+      if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
+      if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
+      trace.mark(1, st);
+      if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+        return cuda_err(e, "sentinel reset");
+      if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
+      if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
+        return s;
+    }
+    if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&] {
+          return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
+                            tg[1].d_prog, fused ? &fb : nullptr);
+        }, &trace, fused ? std::function<qk_status()>([&]() -> qk_status {
+          if (qk_status s = fused_h2d(w, fb.set[0], h_train)) return s;
+          return n_test > 0 ? fused_h2d(w, fb.set[1], h_test) : QK_OK;
+        }) : std::function<qk_status()>()))
+      return s;
+    if (fused) {
+      print_fused_stats(148);
+      if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
+    }
+  }
   static const char* const names[2] = {"train", "test"};
   return check_bad(w->bad, 2, names);
 }

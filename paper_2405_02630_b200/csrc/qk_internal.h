@@ -80,11 +80,13 @@ QK_HD inline int64_t upper_row_offset(int64_t r, int64_t nb) { return r * nb - r
 
 // Device launchers (qk_sweep.cu).  They return QK_OK or a QK_ERR_CUDA status.
 qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
-                            void* d_planes, uint64_t* d_bad, void* stream);
+                            void* d_planes, uint64_t* d_bad, void* stream,
+                            int64_t blk_begin = 0, int64_t blk_end = -1);
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress = nullptr, const FusedBuild* fused = nullptr);
+                       unsigned int* d_progress = nullptr, const FusedBuild* fused = nullptr,
+                       int64_t head_b = 0);
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
                         int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                         int64_t ld, void* stream);
@@ -100,7 +102,8 @@ enum SweepMode { kModeGram = 0, kModeCross = 1, kModeJob = 2 };
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train = nullptr,
-                     unsigned int* d_prog_cross = nullptr, const FusedBuild* fused = nullptr);
+                     unsigned int* d_prog_cross = nullptr, const FusedBuild* fused = nullptr,
+                     int64_t head_b = 0);
 
 }  // namespace qk
 

@@ -428,6 +428,33 @@ __host__ __device__ __forceinline__ void decode_upper(int64_t g, int64_t nb, int
   }
 }
 
+// Gram tile order with a head: for 0 < B < nb (B a multiple of kGroup) the tiles of the
+// B x B leading block triangle come first (in the grouped order over B blocks), then rows
+// [0, B) restricted to columns [B, nb) (super-rows of kGroup rows, column by column), then the
+// super-rows from B on exactly as decode_upper orders them.  A host pipeline can then sweep
+// the head while the angles of blocks >= B are still uploading.  B = 0: decode_upper.
+__host__ __device__ __forceinline__ void decode_gram(int64_t g, int64_t nb, int64_t B,
+                                                     int64_t& bi, int64_t& bj) {
+  if (B <= 0 || B >= nb) {
+    decode_upper(g, nb, bi, bj);
+    return;
+  }
+  const int64_t head = B * (B + 1) / 2;
+  if (g < head) {
+    decode_upper(g, B, bi, bj);
+    return;
+  }
+  g -= head;
+  const int64_t w = nb - B, strip = B * w;
+  if (g < strip) {
+    const int64_t l = g % (int64_t(kGroup) * w);
+    bj = B + l / kGroup;
+    bi = (g / (int64_t(kGroup) * w)) * kGroup + l % kGroup;
+    return;
+  }
+  decode_upper(g - strip + upper_row_offset(B, nb), nb, bi, bj);
+}
+
 __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows, int64_t nb_cols,
                                             int64_t& bi, int64_t& bj) {
   const int64_t r0 = (g / (kRectGroup * nb_cols)) * kRectGroup;
@@ -479,10 +506,10 @@ __global__ void __launch_bounds__(256) gate_build_kernel(const double* __restric
                                                          int64_t n_samples, int64_t ld,
                                                          int width, int n_pad, int front,
                                                          int half, double2* __restrict__ planes,
-                                                         unsigned long long* bad) {
+                                                         unsigned long long* bad, int64_t blk0) {
   __shared__ double tile[kTile][33];
   build_plane_slab<false, 32>(X, n_samples, ld, width, n_pad, front, half, planes, bad,
-                              blockIdx.x, blockIdx.y * 32, tile);
+                              blk0 + blockIdx.x, blockIdx.y * 32, tile);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -523,6 +550,7 @@ struct SweepArgs {
   unsigned long long* stats;  // diagnostics (QK_FUSED_STATS=1): per CTA ns in ensure, t0, t_end
   unsigned long long* next_tile;  // dynamic tile claims beyond the first wave (zeroed per launch)
   int64_t n_split;  // the last n_split tiles run as two row halves each (finer last wave)
+  int64_t head_b;   // Gram tile order with a B-block head (decode_gram; 0: decode_upper)
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -727,7 +755,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       const int64_t g = a.tile_begin + c.t;
       int64_t bi, bj;
       if (MODE == kModeGram || (MODE == kModeJob && g < a.n_first)) {
-        decode_upper(g, a.nb_rows, bi, bj);
+        decode_gram(g, a.nb_rows, a.head_b, bi, bj);
       } else if (MODE == kModeCross) {
         decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
       } else {
@@ -1356,12 +1384,15 @@ static int sm_count() {
 }
 
 qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
-                            void* d_planes, uint64_t* d_bad, void* stream) {
+                            void* d_planes, uint64_t* d_bad, void* stream, int64_t blk_begin,
+                            int64_t blk_end) {
   if (n == 0) return QK_OK;
-  dim3 grid(unsigned(blocks_for(n)), unsigned((p.width_padded + 31) / 32));
+  if (blk_end < 0 || blk_end > blocks_for(n)) blk_end = blocks_for(n);
+  if (blk_end <= blk_begin) return QK_OK;
+  dim3 grid(unsigned(blk_end - blk_begin), unsigned((p.width_padded + 31) / 32));
   gate_build_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       d_angles, n, ld, p.width, p.width_padded, p.front_pad, p.layers == 2 ? 0 : 1,
-      static_cast<double2*>(d_planes), reinterpret_cast<unsigned long long*>(d_bad));
+      static_cast<double2*>(d_planes), reinterpret_cast<unsigned long long*>(d_bad), blk_begin);
   return cuda_status(cudaGetLastError(), "gate_build launch");
 }
 
@@ -1549,11 +1580,14 @@ static void set_fused(SweepArgs& a, const Plan& p, const FusedBuild* fb, int row
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress, const FusedBuild* fused) {
+                       unsigned int* d_progress, const FusedBuild* fused, int64_t head_b) {
   if (tile_end <= tile_begin) return QK_OK;
   if (fused != nullptr && p.layers > 2)
     return set_error(QK_ERR_VALUE, "in-kernel plane build needs layers <= 2");
+  if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
+    return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
   SweepArgs a{};
+  if (mode == kModeGram) a.head_b = head_b;
   if (mode == kModeGram) set_fused(a, p, fused, 0, 0, 0);
   else set_fused(a, p, fused, 0, 1, 0);
   a.progress = d_progress;
@@ -1614,10 +1648,12 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train,
-                     unsigned int* d_prog_cross, const FusedBuild* fused) {
+                     unsigned int* d_prog_cross, const FusedBuild* fused, int64_t head_b) {
   if (tile_end <= tile_begin) return QK_OK;
   if (fused != nullptr && p.layers > 2)
     return set_error(QK_ERR_VALUE, "in-kernel plane build needs layers <= 2");
+  if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
+    return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
   const int64_t nbt = blocks_for(n_train);
   const int64_t n_gram = nbt * (nbt + 1) / 2;
   if (p.layers >= 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
@@ -1631,7 +1667,7 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
     if (qk_status s = launch_sweep(p, kModeGram, d_train, n_train, d_train, n_train, tile_begin,
                                    std::min(tile_end, n_gram), d_K_train, n_train,
                                    QK_OUT_DENSE, stream, d_prog_train,
-                                   fused ? &gram_fb : nullptr))
+                                   fused ? &gram_fb : nullptr, head_b))
       return s;
     if (n_test == 0 || tile_end <= n_gram) return QK_OK;
     return launch_sweep(p, kModeCross, d_test, n_test, d_train, n_train,
@@ -1641,6 +1677,7 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
   }
   SweepArgs a{};
   set_fused(a, p, fused, 0, 0, 1);
+  a.head_b = head_b;
   a.rows = static_cast<const double2*>(d_train);
   a.cols = static_cast<const double2*>(d_train);
   a.n_rows = n_train;

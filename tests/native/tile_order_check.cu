@@ -17,6 +17,15 @@ int main() {
     // panel alignment: tiles of super-row rows [r0, r0+8) occupy [row_off(r0), row_off(r0+8))
     for (int64_t r0 = 0; r0 < nb; r0 += qk::kGroup) { int64_t r1 = std::min<int64_t>(r0 + qk::kGroup, nb);
       for (int64_t g = qk::upper_row_offset(r0, nb); g < qk::upper_row_offset(r1, nb); ++g) { int64_t bi, bj; qk::decode_upper(g, nb, bi, bj); if (bi < r0 || bi >= r1) ok = false; } }
+    // head-first order (decode_gram): a bijection for every head size; the head's tiles are
+    // exactly the B x B leading triangle
+    for (int64_t B = qk::kGroup; B < nb; B += qk::kGroup) {
+      std::set<std::pair<int64_t,int64_t>> s3;
+      for (int64_t g = 0; g < nt; ++g) { int64_t bi, bj; qk::decode_gram(g, nb, B, bi, bj);
+        if (!(0 <= bi && bi <= bj && bj < nb)) ok = false;
+        if ((g < B * (B + 1) / 2) != (bj < B)) ok = false;
+        s3.insert({bi,bj}); }
+      if ((int64_t)s3.size() != nt) ok = false; }
     printf("nb=%ld %s\n", (long)nb, ok ? "ok" : "FAIL");
   }
 }

@@ -390,3 +390,27 @@ def test_empty_cross_blocks_and_joint_pass():
     K, Kx = compute_kernel_matrices(X, np.zeros((0, 5)), cfg)
     assert K.entries.shape == (7, 7) and Kx.entries.shape == (0, 7)
     assert np.abs(K.entries - oracle.kernel_matrix(X, 2)).max() <= K_ABS
+
+
+@pytest.mark.parametrize("n,n_train,n_test", [(784, 2000, 300), (200, 6000, 0), (64, 9000, 777)])
+def test_pinned_head_first_pipeline_matches_pageable(n, n_train, n_test, rng):
+    """Pinned host inputs take the head-first pipeline (the B-block Gram head is swept while
+    the rest of the angles upload); it must equal the pageable path bit for bit."""
+    from paper_2405_02630_b200 import compute_kernel_matrices
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+        t[...] = a
+        return t
+
+    X = rng.uniform(0, np.pi, n) + rng.normal(0, 0.3 / np.sqrt(n), (n_train, n))
+    T = rng.uniform(0, np.pi, n) + rng.normal(0, 0.3 / np.sqrt(n), (n_test, n))
+    cfg = FeatureMapConfig(n)
+    K, Kx = compute_kernel_matrices(X, T, cfg)
+    Kp, Kxp = compute_kernel_matrices(pinned(X), pinned(T), cfg,
+                                      out_train=pinned(np.zeros((n_train, n_train))),
+                                      out_test=pinned(np.zeros((n_test, n_train))))
+    assert np.array_equal(K.entries, Kp.entries)
+    assert np.array_equal(Kx.entries, Kxp.entries)
+    i = rng.integers(0, n_train, 24)
+    assert np.abs(K.entries[np.ix_(i, i)] - oracle.kernel_matrix(X[i], 2)).max() <= K_ABS
