@@ -412,5 +412,9 @@ def test_pinned_head_first_pipeline_matches_pageable(n, n_train, n_test, rng):
                                       out_test=pinned(np.zeros((n_test, n_train))))
     assert np.array_equal(K.entries, Kp.entries)
     assert np.array_equal(Kx.entries, Kxp.entries)
+    Kq, Kxq = compute_kernel_matrices(pinned(X), pinned(T), cfg)  # pageable outputs
+    assert np.array_equal(K.entries, Kq.entries) and np.array_equal(Kx.entries, Kxq.entries)
+    Kg = compute_kernel_matrix(pinned(X), cfg)  # Gram-only entry: the joint pipeline
+    assert np.array_equal(K.entries, Kg.entries)
     i = rng.integers(0, n_train, 24)
     assert np.abs(K.entries[np.ix_(i, i)] - oracle.kernel_matrix(X[i], 2)).max() <= K_ABS
