@@ -51,9 +51,8 @@ constexpr uint32_t kChunkBytes = kChunkElems * 16;     // 16 KB
 // qubits unrolled per inner iteration (tuning knob; config-4 bench with RI = 2: 1 -> 1.175,
 // 2 -> 1.212, 4 -> 1.222, 8 -> 1.233, 16 -> 1.215 G entries/s)
 constexpr int kQUnroll = QK_QUNROLL;
-constexpr int kTileTable = 512;  // per-CTA decoded tile coordinates cached in shared memory
-constexpr size_t kSmemBytes =  // ring, barriers + release counters, tile table, epilogue stage
-    size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8 + kTileTable * 8 +
+constexpr size_t kSmemBytes =  // ring, barriers + release counters, epilogue stage
+    size_t(kStages) * 2 * kChunkBytes + 2 * kStages * 8 +
     size_t(kTile) * (kTile + 1) * 8;
 
 static_assert(kRJ * kTX == kTile, "tile mapping");
@@ -734,8 +733,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   // blocks of tile k + kLook + 1), so that tile is claimed too
   const int kClaim = kLook + (FUSED ? 1 : 0);
   __shared__ Claim ring[8];
-  int2* table = reinterpret_cast<int2*>(released + 2 * kStages);
-  double* stage_T = reinterpret_cast<double*>(table + kTileTable);  // epilogue staging tile
+  double* stage_T = reinterpret_cast<double*>(released + 2 * kStages);  // epilogue staging tile
   // Work items: tiles [0, n_tiles - n_split) whole, then the last n_split tiles as two row
   // halves each, so the final wave ends in half-tile steps (a half tile takes about half the
   // time: the warps of the other half skip the sweep like padding rows do).
