@@ -10,9 +10,15 @@ namespace qk {
 
 // Sweep geometry shared by the planner, the gate-build kernel and the sweep kernels.
 constexpr int kTile = 64;    // samples per plane block == tile edge T
-constexpr int kChunk = 16;   // qubits per bulk-copy chunk Q
-constexpr int kStages = 4;   // shared-memory ring depth
-constexpr int kRescaleChunks = 32;  // L=2: multiply the bond state by 2^-512 every 512 qubits
+#ifndef QK_CHUNK
+#define QK_CHUNK 16
+#endif
+#ifndef QK_STAGES
+#define QK_STAGES 4
+#endif
+constexpr int kChunk = QK_CHUNK;    // qubits per bulk-copy chunk Q
+constexpr int kStages = QK_STAGES;  // shared-memory ring depth
+constexpr int kRescaleChunks = 512 / kChunk;  // L=2: rescale the bond state by 2^-512 every 512 qubits
 constexpr int kMaxLayers = 8;       // L <= 4: registers; L = 5..8: shared-memory deep sweep
 constexpr int kGroup = 8;           // tile rows per super-row of the L2-friendly tile order
 #ifndef QK_RECT_GROUP
