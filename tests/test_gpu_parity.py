@@ -418,3 +418,22 @@ def test_pinned_head_first_pipeline_matches_pageable(n, n_train, n_test, rng):
     assert np.array_equal(K.entries, Kg.entries)
     i = rng.integers(0, n_train, 24)
     assert np.abs(K.entries[np.ix_(i, i)] - oracle.kernel_matrix(X[i], 2)).max() <= K_ABS
+
+
+def test_kernel_job_graph_replay_matches_run(rng):
+    """KernelJob.graph: a CUDA-graph replay of the job recomputes the same matrices, also
+    after the input tensors are refilled in place."""
+    n, N, M = 24, 300, 70
+    tr = torch.as_tensor(rng.uniform(0, np.pi, (N, n)), device="cuda")
+    te = torch.as_tensor(rng.uniform(0, np.pi, (M, n)), device="cuda")
+    job = KernelJob(SweepPlan(n, 2), N, M)
+    replay, K, Kx = job.graph(tr, te)
+    replay()
+    torch.cuda.synchronize()
+    K0, Kx0 = KernelJob(SweepPlan(n, 2), N, M).run(tr, te)
+    assert torch.equal(K, K0) and torch.equal(Kx, Kx0)
+    tr.copy_(torch.as_tensor(rng.uniform(0, np.pi, (N, n)), device="cuda"))
+    replay()
+    torch.cuda.synchronize()
+    K1, _ = KernelJob(SweepPlan(n, 2), N, M).run(tr, te)
+    assert torch.equal(K, K1)
