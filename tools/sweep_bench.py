@@ -11,7 +11,6 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2405_02630_b200 import SweepPlan  # noqa: E402
-from paper_2405_02630_b200 import device as dev  # noqa: E402
 from paper_2405_02630_b200.distributed import KernelJob  # noqa: E402
 
 
