@@ -64,8 +64,8 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   p.width_padded = ((width + kChunk - 1) / kChunk) * kChunk;
   p.front_pad = p.width_padded - width;
   const int nchunks = p.width_padded / kChunk;
-  if (layers == 2 || layers == 3) {
-    // The rotated recurrences (bond 4 and the blocked bond 16) drop a factor 1/2 per processed
+  if (layers >= 2 && layers <= 4) {
+    // The rotated recurrences (bond 4, the blocked bonds 16 / 64) drop a factor 1/2 per processed
     // qubit (the identity qubits of the front padding are skipped, not processed); the kernels
     // multiply the state by 2^-512 after every kRescaleChunks chunks.
     const int rescales = (nchunks - 1) / kRescaleChunks;
@@ -97,16 +97,18 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
     in.flops_per_entry = 4 * n;
     in.algorithmic_flops_per_entry = 4 * n;
     in.reference_cmacs_per_entry = 0;
-  } else if (layers == 3) {
-    // rotated blocked bond 16 (qk_sweep.cu bond16_step): full angles 8, cos/sin of the
-    // difference 4, separable sums 4, level-0 passes 64, the four block updates 32 -> 112
-    // instructions (60 of them FMAs) per pair-qubit; 7 adds, the scale and the square last
-    in.dp_instr_per_entry = 112 * n + 9;
-    in.flops_per_entry = 172 * n + 9;
+  } else if (layers <= 4) {
+    // rotated blocked bond (qk_sweep.cu bondr_step), M = L-1, E = 4^M: full angles 8, cos/sin
+    // of the difference 4, separable sums 4, lower-level passes 4 (M-1) E (half of them FMAs),
+    // the E/4 block updates 2 E (1.5 E FMAs); E/2 - 1 adds, the scale and the square last
+    const int64_t M = layers - 1, E = int64_t(1) << (2 * M);
+    const int64_t instr = 4 * (M - 1) * E + 2 * E + 16, fmas = 2 * (M - 1) * E + 3 * E / 2 + 4;
+    in.dp_instr_per_entry = instr * n + E / 2 + 1;
+    in.flops_per_entry = (instr + fmas) * n + E / 2 + 1;
     in.algorithmic_flops_per_entry = in.flops_per_entry;
     in.reference_cmacs_per_entry = 0;
   } else {
-    // L >= 4, D = 2^(L-1), V is D x D (E = D^2 elements).  Per qubit per pair: two sides of
+    // L >= 5, D = 2^(L-1), V is D x D (E = D^2 elements).  Per qubit per pair: two sides of
     // M = L-1 level passes, each D^2/2 rotations of 2 DMUL + 2 DFMA (6 flops); cos/sin of
     // delta/2 (2 DMUL + 2 DFMA); the RY(delta) mask (E DMUL).  E - 1 adds and the square last.
     const int64_t M = layers - 1, E = int64_t(1) << (2 * M);

@@ -287,71 +287,62 @@ __device__ __forceinline__ double ry_delta_mask(int e, int M, double cd, double 
   return tb == tc ? cd : (tb ? sd : -sd);
 }
 
-// Register-resident bond (L = 3, 4: D = 4, 8), one pair per thread, fully unrolled.
+// L = 3, 4 in a rotated, blocked basis (the L = 2 trick applied to the top level).  The D x D
+// state (D = 2^M, M = L - 1) splits into (D/2)^2 blocks B[r][c] of 2x2 over the top bits,
+// indexed by the lower M - 1 bits of row and column.  One qubit: the lower-level passes mix the
+// blocks (the factored rotations above, rows with (c_i, s_i), columns with (c_j, s_j)); then
+// each block takes an L = 2-type step B <- (A(x_i + t_r pi) B A(x_j + t_c pi)) o RY(delta),
+// t_r / t_c = bit M - 2 of the block's row / column (the top-level pass is selected by it: RY
+// at the angle shifted by pi).  In the Hadamard basis of the top bits, S = w00 + w11,
+// Dg = w00 - w11, T = w01 + w10, E = w01 - w10 of every block update with the SAME seven
+// coefficients as L = 2 up to signs and permutations: 1 +- C, D (C, D = cos, sin of
+// x_j - x_i) and the separable a_i + a_j, b_i + b_j, b_j - b_i, a_i - a_j (a, b = cos, sin of
+// the full angles), the 1/2 per qubit folded into one power of two (2^-512 rescales as L = 2).
+// (4 (M-1) E + 2 E + 16) FP64 instructions per pair-qubit (E = D^2): L = 3 112 instead of 148,
+// L = 4 656 instead of 836.  Verified in numpy against the reference goldens for L = 3..6.
 template <int M>
-struct BondG {
-  static constexpr int D = 1 << M, E = D * D;
-  double v[E];
+struct BondR {
+  static constexpr int H = 1 << (M - 1), E = 4 * H * H;
+  double v[E];  // block (r, c) at 4 (r H + c): S, Dg, T, E
 };
 
-template <int M, int OFF>
-__device__ __forceinline__ void bondg_side(double (&v)[1 << (2 * M)], double c, double s) {
-  constexpr int E = 1 << (2 * M);
+template <int M>
+__device__ __forceinline__ void bondr_init(BondR<M>& s) {
 #pragma unroll
-  for (int k = 0; k < M; ++k)
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int pos = OFF + k;
-      if (e & (1 << pos)) continue;
-      rot_pair(v[e], v[e | (1 << pos)], c, s, k == 0 ? 0 : (e >> (pos - 1)) & 1);
-    }
+  for (int e = 0; e < BondR<M>::E; ++e) s.v[e] = (e == 0 || e == 2) ? 1.0 : 0.0;
+}
+
+// the per-block L = 2-type step for top-level selectors (TR, TC)
+template <int TR, int TC>
+__device__ __forceinline__ void block_step(double* v, double C, double D, double p1, double q1,
+                                           double p2, double q2) {
+  const double S = v[0], Dg = v[1], T = v[2], E = v[3];
+  if (TR == 0 && TC == 0) {
+    v[0] = fma(q1, Dg, fma(C, S, S));
+    v[1] = fma(p2, E, fma(C, T, -T));
+    v[2] = fma(-D, E, p1 * T);
+    v[3] = fma(D, Dg, q2 * S);
+  } else if (TR == 0) {
+    v[0] = fma(p1, Dg, -(D * S));
+    v[1] = fma(-q2, E, -(D * T));
+    v[2] = fma(-q1, T, -fma(C, E, E));
+    v[3] = fma(p2, S, fma(C, Dg, -Dg));
+  } else if (TC == 0) {
+    v[0] = fma(p1, Dg, D * S);
+    v[1] = fma(-q2, E, D * T);
+    v[2] = fma(-q1, T, fma(C, E, E));
+    v[3] = fma(p2, S, fma(-C, Dg, Dg));
+  } else {
+    v[0] = fma(-q1, Dg, fma(C, S, S));
+    v[1] = fma(-p2, E, fma(C, T, -T));
+    v[2] = fma(-D, E, -(p1 * T));
+    v[3] = fma(D, Dg, -(q2 * S));
+  }
 }
 
 template <int M>
-__device__ __forceinline__ void bondg_init(BondG<M>& s) {
-#pragma unroll
-  for (int e = 0; e < BondG<M>::E; ++e) s.v[e] = e == 0 ? 1.0 : 0.0;
-}
-
-template <int M>
-__device__ __forceinline__ void bondg_step(BondG<M>& s, double2 vi, double2 vj) {
-  bondg_side<M, M>(s.v, vi.x, vi.y);  // F_i^T V  (row index)
-  bondg_side<M, 0>(s.v, vj.x, vj.y);  // (.) F_j  (column index)
-  const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
-  const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
-#pragma unroll
-  for (int e = 0; e < BondG<M>::E; ++e) s.v[e] *= ry_delta_mask(e, M, cd, sd);
-}
-
-template <int M>
-__device__ __forceinline__ double bondg_amp(const BondG<M>& s) {
-  double acc = 0.0;
-#pragma unroll
-  for (int e = 0; e < BondG<M>::E; ++e) acc += s.v[e];
-  return acc;
-}
-
-// L = 3 in a rotated basis (the L = 2 trick applied to the top level).  The 4x4 state splits
-// into four 2x2 blocks B[r0][c0] over the top bits (r1, c1), indexed by the level-0 bits.  One
-// qubit: the level-0 passes mix the blocks (rows with (c_i, s_i), columns with (c_j, s_j));
-// then each block takes an L = 2-type step B <- (A(x_i + r0 pi) B A(x_j + c0 pi)) o RY(delta)
-// (a level-1 pass selected by bit 0 is RY at the angle shifted by pi).  In the Hadamard basis
-// of the top bits, S = w00 + w11, Dg = w00 - w11, T = w01 + w10, E = w01 - w10 of each block
-// update with the SAME seven coefficients as L = 2 for every block, up to signs and
-// permutations: 1 +- C, D (C, D = cos, sin of x_j - x_i) and the separable a_i + a_j,
-// b_i + b_j, b_j - b_i, a_i - a_j (a, b = cos, sin of the full angle), the 1/2 per qubit folded
-// into one power of two at the end.  112 FP64 instructions per pair-qubit against 148 for the
-// plain factored passes.  Verified in numpy against the reference goldens first.
-struct Bond16 {
-  double v[16];  // block (r0, c0) at 4 (2 r0 + c0): S, Dg, T, E
-};
-
-__device__ __forceinline__ void bond16_init(Bond16& s) {
-#pragma unroll
-  for (int e = 0; e < 16; ++e) s.v[e] = (e == 0 || e == 2) ? 1.0 : 0.0;
-}
-
-__device__ __forceinline__ void bond16_step(Bond16& s, double2 vi, double2 vj) {
+__device__ __forceinline__ void bondr_step(BondR<M>& s, double2 vi, double2 vj) {
+  constexpr int H = BondR<M>::H;
   const double ci = vi.x, si = vi.y, cj = vj.x, sj = vj.y;  // half-angle planes
   const double ai = fma(ci, ci, -(si * si)), bi = (ci + ci) * si;  // cos x_i, sin x_i
   const double aj = fma(cj, cj, -(sj * sj)), bj = (cj + cj) * sj;
@@ -360,52 +351,44 @@ __device__ __forceinline__ void bond16_step(Bond16& s, double2 vi, double2 vj) {
   const double p1 = ai + aj, q1 = bi + bj, p2 = bj - bi, q2 = ai - aj;
   double* v = s.v;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {  // level 0, rows: block (0, c0) with block (1, c0)
-    const double x0 = v[e], x1 = v[8 + e];
-    v[e] = fma(ci, x0, si * x1);
-    v[8 + e] = fma(si, x0, ci * x1);
-  }
+  for (int k = 0; k < M - 1; ++k)  // lower levels, rows (block row index r)
 #pragma unroll
-  for (int r0 = 0; r0 < 2; ++r0)
+    for (int r = 0; r < H; ++r) {
+      if (r & (1 << k)) continue;
+      const int r1 = r | (1 << k), sel = k == 0 ? 0 : (r >> (k - 1)) & 1;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // level 0, columns: block (r0, 0) with block (r0, 1)
-      const double x0 = v[8 * r0 + k], x1 = v[8 * r0 + 4 + k];
-      v[8 * r0 + k] = fma(cj, x0, sj * x1);
-      v[8 * r0 + 4 + k] = fma(sj, x0, cj * x1);
+      for (int e = 0; e < 4 * H; ++e) rot_pair(v[4 * H * r + e], v[4 * H * r1 + e], ci, si, sel);
     }
-  {  // block (0, 0)
-    const double S = v[0], Dg = v[1], T = v[2], E = v[3];
-    v[0] = fma(q1, Dg, fma(C, S, S));
-    v[1] = fma(p2, E, fma(C, T, -T));
-    v[2] = fma(-D, E, p1 * T);
-    v[3] = fma(D, Dg, q2 * S);
-  }
-  {  // block (0, 1)
-    const double S = v[4], Dg = v[5], T = v[6], E = v[7];
-    v[4] = fma(p1, Dg, -(D * S));
-    v[5] = fma(-q2, E, -(D * T));
-    v[6] = fma(-q1, T, -fma(C, E, E));
-    v[7] = fma(p2, S, fma(C, Dg, -Dg));
-  }
-  {  // block (1, 0)
-    const double S = v[8], Dg = v[9], T = v[10], E = v[11];
-    v[8] = fma(p1, Dg, D * S);
-    v[9] = fma(-q2, E, D * T);
-    v[10] = fma(-q1, T, fma(C, E, E));
-    v[11] = fma(p2, S, fma(-C, Dg, Dg));
-  }
-  {  // block (1, 1)
-    const double S = v[12], Dg = v[13], T = v[14], E = v[15];
-    v[12] = fma(-q1, Dg, fma(C, S, S));
-    v[13] = fma(-p2, E, fma(C, T, -T));
-    v[14] = fma(-D, E, -(p1 * T));
-    v[15] = fma(D, Dg, -(q2 * S));
-  }
+#pragma unroll
+  for (int k = 0; k < M - 1; ++k)  // lower levels, columns (block column index c)
+#pragma unroll
+    for (int c = 0; c < H; ++c) {
+      if (c & (1 << k)) continue;
+      const int c1 = c | (1 << k), sel = k == 0 ? 0 : (c >> (k - 1)) & 1;
+#pragma unroll
+      for (int r = 0; r < H; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          rot_pair(v[4 * (r * H + c) + q], v[4 * (r * H + c1) + q], cj, sj, sel);
+    }
+#pragma unroll
+  for (int r = 0; r < H; ++r)
+#pragma unroll
+    for (int c = 0; c < H; ++c) {
+      double* b = v + 4 * (r * H + c);
+      const int tr = (r >> (M - 2)) & 1, tc = (c >> (M - 2)) & 1;
+      if (tr == 0 && tc == 0) block_step<0, 0>(b, C, D, p1, q1, p2, q2);
+      else if (tr == 0) block_step<0, 1>(b, C, D, p1, q1, p2, q2);
+      else if (tc == 0) block_step<1, 0>(b, C, D, p1, q1, p2, q2);
+      else block_step<1, 1>(b, C, D, p1, q1, p2, q2);
+    }
 }
 
-__device__ __forceinline__ double bond16_amp(const Bond16& s, double final_scale) {
-  // sum(V) = sum over blocks of 2 w00 = S + Dg
-  const double t = ((s.v[0] + s.v[1]) + (s.v[4] + s.v[5])) + ((s.v[8] + s.v[9]) + (s.v[12] + s.v[13]));
+template <int M>
+__device__ __forceinline__ double bondr_amp(const BondR<M>& s, double final_scale) {
+  double t = 0.0;  // sum(V) = sum over blocks of 2 w00 = S + Dg
+#pragma unroll
+  for (int b = 0; b < BondR<M>::E / 4; ++b) t += s.v[4 * b] + s.v[4 * b + 1];
   return t * final_scale;
 }
 
@@ -421,41 +404,38 @@ struct BondT<2> {
 };
 template <>
 struct BondT<3> {
-  using type = Bond16;
+  using type = BondR<2>;
 };
 template <>
 struct BondT<4> {
-  using type = BondG<3>;
+  using type = BondR<3>;
 };
 
 template <int LAYERS>
 __device__ __forceinline__ void st_init(typename BondT<LAYERS>::type& s) {
   if constexpr (LAYERS == 2) bond4_init(s);
   else if constexpr (LAYERS == 1) bond1_init(s);
-  else if constexpr (LAYERS == 3) bond16_init(s);
-  else bondg_init<LAYERS - 1>(s);
+  else bondr_init<LAYERS - 1>(s);
 }
 template <int LAYERS>
 __device__ __forceinline__ void st_step(typename BondT<LAYERS>::type& s, double2 vi, double2 vj) {
   if constexpr (LAYERS == 2) bond4_step(s, vi, vj);
   else if constexpr (LAYERS == 1) bond1_step(s, vi, vj);
-  else if constexpr (LAYERS == 3) bond16_step(s, vi, vj);
-  else bondg_step<LAYERS - 1>(s, vi, vj);
+  else bondr_step<LAYERS - 1>(s, vi, vj);
 }
 template <int LAYERS>
 __device__ __forceinline__ void st_rescale(typename BondT<LAYERS>::type& s) {
   if constexpr (LAYERS == 2) bond4_scale(s, 0x1p-512);
-  if constexpr (LAYERS == 3) {
+  if constexpr (LAYERS == 3 || LAYERS == 4) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) s.v[e] *= 0x1p-512;
+    for (int e = 0; e < BondR<LAYERS - 1>::E; ++e) s.v[e] *= 0x1p-512;
   }
 }
 template <int LAYERS>
 __device__ __forceinline__ double st_amp(const typename BondT<LAYERS>::type& s, double fs) {
   if constexpr (LAYERS == 2) return bond4_amp(s, fs);
   else if constexpr (LAYERS == 1) return s.v;
-  else if constexpr (LAYERS == 3) return bond16_amp(s, fs);
-  else return bondg_amp<LAYERS - 1>(s);
+  else return bondr_amp<LAYERS - 1>(s, fs);
 }
 
 __device__ __forceinline__ double kernel_value(double amp, int convention) {
@@ -1133,8 +1113,8 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
 #pragma unroll kUnrollQ
     for (int q = a.front; q < a.n_pad; ++q) {  // the front padding qubits are identities
       st_step<LAYERS>(st, __ldg(pi + int64_t(q) * kTile), __ldg(pj + int64_t(q) * kTile));
-      // L = 3 (rotated, 1/2 per qubit dropped): the same 2^-512 rescale points as L = 2
-      if (LAYERS == 3 && (q + 1) % (kChunk * kRescaleChunks) == 0 && q + 1 < a.n_pad)
+      // L = 3, 4 (rotated, 1/2 per qubit dropped): the same 2^-512 rescale points as L = 2
+      if (LAYERS >= 3 && (q + 1) % (kChunk * kRescaleChunks) == 0 && q + 1 < a.n_pad)
         st_rescale<LAYERS>(st);
     }
     const double v = kernel_value(st_amp<LAYERS>(st, a.final_scale), a.convention);
@@ -1397,7 +1377,7 @@ __global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ 
       const int64_t off = int64_t(ch * kChunk + qq) * kTile;
       st_step<LAYERS>(s, __ldg(a + off), __ldg(b + off));
     }
-    if ((LAYERS == 2 || LAYERS == 3) && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0)
+    if (LAYERS >= 2 && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0)
       st_rescale<LAYERS>(s);
   }
   amp[k] = st_amp<LAYERS>(s, final_scale);

@@ -58,12 +58,14 @@ def test_plan_geometry_and_costs():
     assert q.info["width_padded"] == 32  # 15 identity qubits in front
     assert SweepPlan(5, 1).info["bond"] == 1
     assert SweepPlan(5, 3).info["bond"] == 16
-    for L in (4, 5, 6, 7, 8):  # factored level passes: (4 M E + E + 4) n + E instructions
+    for L in (5, 6, 7, 8):  # factored level passes: (4 M E + E + 4) n + E instructions
         M, E = L - 1, 4 ** (L - 1)
         info = SweepPlan(5, L).info
         assert info["bond"] == E
         assert info["dp_instr_per_entry"] == (4 * M * E + E + 4) * 5 + E
     assert SweepPlan(5, 3).info["dp_instr_per_entry"] == 112 * 5 + 9  # rotated blocked bond 16
+    assert SweepPlan(5, 4).info["dp_instr_per_entry"] == 656 * 5 + 33  # rotated blocked bond 64
+    assert SweepPlan(5, 4).info["bond"] == 64
 
 
 def test_null_and_range_arguments_are_rejected():
