@@ -29,8 +29,11 @@ KEYS = [
 
 
 def rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):  # a raw page exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     h, units = r[0], r[1]
     for v in r[2:]:

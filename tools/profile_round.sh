@@ -19,3 +19,8 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:swee
 ./tools/dmma_bench > gpurun_out/dmma_$TAG.txt 2>&1
 timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 echo done
+# keep the copy-back under gpurun's 64 MiB: raw pages as CSV, the reports themselves dropped
+for k in sweep gate deep general; do
+  [ -f gpurun_out/prof_${k}_$TAG.ncu-rep ] && ncu -i gpurun_out/prof_${k}_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_${k}_${TAG}_raw.csv 2>/dev/null
+done
+rm -f gpurun_out/*.ncu-rep
