@@ -59,6 +59,7 @@ class JobLayout:
     cross_tiles: int
     world: int
     tile_elems: int
+    bounds: tuple = ()  # world + 1 tile-list boundaries (cost-balanced); () = equal counts
 
     @property
     def total_tiles(self) -> int:
@@ -66,9 +67,13 @@ class JobLayout:
 
     @property
     def range_len(self) -> int:
-        return ceil(self.total_tiles / self.world) if self.total_tiles else 0
+        if not self.total_tiles:
+            return 0
+        return max(hi - lo for lo, hi in (self.union_range(r) for r in range(self.world)))
 
     def union_range(self, rank: int) -> tuple[int, int]:
+        if self.bounds:
+            return self.bounds[rank], self.bounds[rank + 1]
         return shard_range(self.total_tiles, rank, self.world)
 
     def segments(self, rank: int) -> list[Segment]:
@@ -88,10 +93,46 @@ class JobLayout:
         return self.n_train * (self.n_train - 1) // 2 + self.n_test * self.n_train
 
 
+def _pad(n: int, edge: int) -> int:
+    return (edge - n % edge) % edge
+
+
+def tile_costs(n_train: int, n_test: int, edge: int, group: int = 8) -> np.ndarray:
+    """Relative sweep cost of every tile of the joint list (Gram in the kernel's grouped order,
+    then cross row-major; qk_sweep.cu decode_upper / decode_rect): 1, except the tiles of
+    tile row 0, whose front padding rows skip the sweep in whole 4-row warps (16 real rows of
+    64 cost ~1/4 of a tile, measured)."""
+    nb = -(-n_train // edge) if n_train else 0
+    nbt = -(-n_test // edge) if n_test else 0
+    w = np.ones(nb * (nb + 1) // 2 + nbt * nb)
+    def row0_weight(n):
+        pad = _pad(n, edge)
+        return -(-(edge - pad) // 4) / (edge // 4)
+    if nb:
+        h = min(group, nb)
+        cols = np.arange(nb)
+        idx = np.where(cols < h, cols * (cols + 1) // 2, h * (h + 1) // 2 + h * (cols - h))
+        w[idx] = row0_weight(n_train)  # Gram tile row 0 lies in super-row 0
+    if nbt:
+        g0 = nb * (nb + 1) // 2
+        w[g0:g0 + nb] = row0_weight(n_test)  # cross tile row 0 (test block 0)
+    return w
+
+
 def layout_for(plan: SweepPlan, n_train: int, n_test: int, world: int) -> JobLayout:
-    return JobLayout(n_train, n_test, plan.gram_tile_count(n_train),
-                     plan.cross_tile_count(n_test, n_train) if n_test else 0, world,
-                     plan.tile_edge * plan.tile_edge)
+    """The job's tile list split into contiguous per-rank ranges of equal estimated COST
+    (tile_costs): the ranks holding the cheap padding tile rows take more tiles."""
+    edge = plan.tile_edge
+    gram = plan.gram_tile_count(n_train)
+    cross = plan.cross_tile_count(n_test, n_train) if n_test else 0
+    bounds = ()
+    if world > 1 and gram + cross:
+        cum = np.concatenate([[0.0], np.cumsum(tile_costs(n_train, n_test, edge))])
+        targets = cum[-1] * np.arange(world + 1) / world
+        b = np.searchsorted(cum, targets, side="left")
+        b[0], b[-1] = 0, gram + cross
+        bounds = tuple(int(x) for x in np.maximum.accumulate(b))
+    return JobLayout(n_train, n_test, gram, cross, world, edge * edge, bounds)
 
 
 def gather_packed(local: torch.Tensor, layout: JobLayout, group=None) -> list | None:

@@ -118,3 +118,22 @@ def test_gather_rebuilds_dense_matrices_world2():
         p.join(timeout=60)
     assert ok == (True, True)
     assert all(p.exitcode == 0 for p in procs)
+
+
+def test_cost_balanced_ranges_cover_the_list_once():
+    """layout_for splits the joint tile list into contiguous ranges of equal estimated cost:
+    they tile the list exactly, and the ranks holding the padding tile rows (cost 1/4) get
+    more tiles."""
+    from paper_2405_02630_b200.distributed import tile_costs
+    plan = SweepPlan(784, 2)
+    for world in (1, 2, 3, 4, 8):
+        lay = layout_for(plan, 10000, 2000, world)
+        rngs = [lay.union_range(r) for r in range(world)]
+        assert rngs[0][0] == 0 and rngs[-1][1] == lay.total_tiles
+        assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
+        cost = tile_costs(10000, 2000, 64)
+        per = [cost[lo:hi].sum() for lo, hi in rngs]
+        assert max(per) - min(per) <= 2.0  # one tile of granularity per boundary
+    lay = layout_for(plan, 10000, 2000, 8)
+    sizes = [hi - lo for lo, hi in (lay.union_range(r) for r in range(8))]
+    assert sizes[0] > sizes[1]  # rank 0 holds the Gram's padding tile row
