@@ -875,29 +875,44 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
     if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st, 0, B))
       return s;
     const int64_t n_head = B * (B + 1) / 2;
+    // The rest (its upload, its gate builds and its sweep) runs on the h2d stream, after the
+    // head planes: its gate-build CTAs and then its sweep CTAs take the SMs as the head
+    // sweep's CTAs retire, so the head's last wave overlaps the rest instead of idling SMs.
+    // The main stream waits for the rest at the end (the drain does not need it: it follows
+    // the tile-row counters).
+    cudaStream_t hs = w->h2d_stream;
+    cudaEvent_t ev[2];
+    for (int k = 0; k < 2; ++k)
+      if (cudaError_t e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming)) {
+        if (k) cudaEventDestroy(ev[0]);
+        return cuda_err(e, "cudaEventCreate");
+      }
+    struct Destroy {
+      cudaEvent_t* ev;
+      ~Destroy() { cudaEventDestroy(ev[0]), cudaEventDestroy(ev[1]); }
+    } destroy{ev};
+    if (cudaError_t e = cudaEventRecord(ev[0], st)) return cuda_err(e, "cudaEventRecord");
     if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&]() -> qk_status {
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, 0, n_head, dKt, dKs, st,
                                         tg[0].d_prog, tg[1].d_prog, nullptr, B))
             return s2;
           cudaError_t e = cudaMemcpyAsync(dXt + s1 * p->width, h_train + s1 * p->width,
                                           size_t(n_train - s1) * row, cudaMemcpyHostToDevice,
-                                          w->h2d_stream);
+                                          hs);
           if (e == cudaSuccess && n_test > 0)
-            e = cudaMemcpyAsync(dXs, h_test, xsb, cudaMemcpyHostToDevice, w->h2d_stream);
-          cudaEvent_t up;
-          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&up, cudaEventDisableTiming);
-          if (e == cudaSuccess) {
-            e = cudaEventRecord(up, w->h2d_stream);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(st, up, 0);
-            cudaEventDestroy(up);
-          }
+            e = cudaMemcpyAsync(dXs, h_test, xsb, cudaMemcpyHostToDevice, hs);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev[0], 0);  // head planes, sentinel
           if (e != cudaSuccess) return cuda_err(e, "H2D rest");
-          if (qk_status s2 = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st, B))
+          if (qk_status s2 = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, hs, B))
             return s2;
-          if (qk_status s2 = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
+          if (qk_status s2 = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, hs))
             return s2;
-          return launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, st,
-                            tg[0].d_prog, tg[1].d_prog, nullptr, B);
+          if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, hs,
+                                        tg[0].d_prog, tg[1].d_prog, nullptr, B))
+            return s2;
+          e = cudaEventRecord(ev[1], hs);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[1], 0);
+          return e == cudaSuccess ? QK_OK : cuda_err(e, "rest sweep join");
         }, &trace))
       return s;
   } else {
