@@ -697,7 +697,11 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
                                  cudaMemcpyDeviceToHost, cs);
       };
       const bool gram = t.mode == kModeGram;
-      const int64_t step = gram ? kGroup : 1;
+      // cross panels: whole tile rows, but at least ~2 MB per copy (small jobs: a 64-row
+      // copy of a narrow matrix is latency-bound)
+      const int64_t row_bytes = kTile * t.n_cols * int64_t(sizeof(double));
+      const int64_t step = gram ? kGroup : std::max<int64_t>(1, ((2 << 20) + row_bytes - 1) /
+                                                                    row_bytes);
       for (int64_t r0 = 0; r0 < nbr && e == cudaSuccess; r0 += step) {
         const int64_t r1 = std::min(r0 + step, nbr);
         for (int64_t q = r0; q < r1 && t.d_prog != nullptr && e == cudaSuccess; ++q) {
