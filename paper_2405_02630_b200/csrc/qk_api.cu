@@ -870,12 +870,12 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
     // head: its angles, its planes, then the head sweep with the rest uploading beside it
     const int64_t s1 = std::min<int64_t>(n_train, B * kTile - sample_pad(n_train));
     const size_t row = size_t(p->width) * sizeof(double);
+    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+      return cuda_err(e, "sentinel reset");
     if (cudaError_t e = cudaMemcpyAsync(dXt, h_train, size_t(s1) * row, cudaMemcpyHostToDevice,
                                         st))
       return cuda_err(e, "H2D head");
     trace.mark(1, st);
-    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
-      return cuda_err(e, "sentinel reset");
     if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st, 0, B))
       return s;
     const int64_t n_head = B * (B + 1) / 2;
