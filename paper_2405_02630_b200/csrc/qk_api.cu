@@ -906,17 +906,23 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
           if (e == cudaSuccess && n_test > 0)
             e = cudaMemcpyAsync(dXs, h_test, xsb, cudaMemcpyHostToDevice, hs);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev[0], 0);  // head planes, sentinel
-          if (e != cudaSuccess) return cuda_err(e, "H2D rest");
+          // on a failure past this point, let the rest's queued work finish before returning
+          // (it reads and writes the workspace the next call reuses)
+          auto fail = [&](qk_status s2) {
+            cudaStreamSynchronize(hs);
+            return s2;
+          };
+          if (e != cudaSuccess) return fail(cuda_err(e, "H2D rest"));
           if (qk_status s2 = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, hs, B))
-            return s2;
+            return fail(s2);
           if (qk_status s2 = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, hs))
-            return s2;
+            return fail(s2);
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, hs,
                                         tg[0].d_prog, tg[1].d_prog, nullptr, B))
-            return s2;
+            return fail(s2);
           e = cudaEventRecord(ev[1], hs);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[1], 0);
-          return e == cudaSuccess ? QK_OK : cuda_err(e, "rest sweep join");
+          return e == cudaSuccess ? QK_OK : fail(cuda_err(e, "rest sweep join"));
         }, &trace))
       return s;
   } else {

@@ -420,6 +420,33 @@ def test_pinned_head_first_pipeline_matches_pageable(n, n_train, n_test, rng):
     assert np.abs(K.entries[np.ix_(i, i)] - oracle.kernel_matrix(X[i], 2)).max() <= K_ABS
 
 
+@pytest.mark.parametrize("where", ["head", "rest", "test"])
+def test_pinned_head_first_non_finite_raises_rebind(where, rng):
+    """A non-finite angle in the head's samples, in the rest (uploaded and gate-built on the
+    second stream beside the head sweep) or in the test set raises the reference's
+    RebindError, and the pipeline is healthy afterwards (same result as before)."""
+    from paper_2405_02630_b200 import RebindError, compute_kernel_matrices
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+        t[...] = a
+        return t
+
+    n, N, M = 784, 3000, 200
+    X = pinned(rng.uniform(0, np.pi, (N, n)))
+    T = pinned(rng.uniform(0, np.pi, (M, n)))
+    cfg = FeatureMapConfig(n)
+    K0, Kx0 = compute_kernel_matrices(X, T, cfg)
+    bad = {"head": (X, 5), "rest": (X, N - 3), "test": (T, M - 1)}[where]
+    old = bad[0][bad[1], 100]
+    bad[0][bad[1], 100] = np.nan
+    with pytest.raises(RebindError, match=r"operand set \d+: feature angles must be finite"):
+        compute_kernel_matrices(X, T, cfg)
+    bad[0][bad[1], 100] = old
+    K1, Kx1 = compute_kernel_matrices(X, T, cfg)
+    assert np.array_equal(K0.entries, K1.entries) and np.array_equal(Kx0.entries, Kx1.entries)
+
+
 def test_kernel_job_graph_replay_matches_run(rng):
     """KernelJob.graph: a CUDA-graph replay of the job recomputes the same matrices, also
     after the input tensors are refilled in place."""
