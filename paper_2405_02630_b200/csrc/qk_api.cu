@@ -398,8 +398,8 @@ StreamWriteValue32Fn stream_write_value32() {
   return fn;
 }
 
-// In-kernel plane build for the host pipelines (L <= 2, pinned angle buffers, stream memory
-// operations available; QK_FUSED_BUILD=0 disables it): the angles go up in chunks of
+// In-kernel plane build for the host pipelines (opt-in, QK_FUSED_BUILD=1; L <= 2, pinned
+// angle buffers, stream memory operations available): the angles go up in chunks of
 // kArriveBlocks plane blocks on w->h2d_stream, each followed by an arrival mark, and the
 // sweep starts at once — its CTAs build each plane block as soon as its chunk has landed, so
 // the H2D of the inputs overlaps the sweep instead of preceding it.
