@@ -1,0 +1,52 @@
+"""Randomised stress of the host pipelines (head-first two-stream overlap, per-tile-row
+drains, pinned / pageable inputs and outputs, in-kernel build on/off) against the
+device-resident path, bit for bit.  usage: python tools/stress_pipelines.py [seconds]"""
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2405_02630_b200 import FeatureMapConfig, compute_kernel_matrices  # noqa: E402
+
+
+def pin(a):
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+    t[...] = a
+    return t
+
+
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300
+rng = np.random.default_rng(int(time.time()))
+t0, cases, entries = time.time(), 0, 0
+while time.time() - t0 < budget:
+    n = int(rng.choice([3, 8, 17, 50, 64, 200, 784]))
+    L = int(rng.choice([1, 2, 2, 2, 3])) if n <= 200 else 2
+    ntr = int(rng.integers(2, 7000 if n >= 200 else 4000))
+    nte = int(rng.integers(0, 2500))
+    X = rng.uniform(0, np.pi, (ntr, n))
+    T = rng.uniform(0, np.pi, (nte, n))
+    cfg = FeatureMapConfig(n, layers=L)
+    Kd, Kxd = compute_kernel_matrices(torch.as_tensor(X, device="cuda"),
+                                      torch.as_tensor(T, device="cuda"), cfg)
+    Kd, Kxd = Kd.entries.cpu().numpy(), Kxd.entries.cpu().numpy()
+    pin_in, pin_out = bool(rng.integers(2)), bool(rng.integers(2))
+    os.environ["QK_FUSED_BUILD"] = "1" if rng.integers(4) == 0 else "0"
+    Xi, Ti = (pin(X), pin(T)) if pin_in else (X, T)
+    kw = {}
+    if pin_out:
+        kw = {"out_train": pin(np.full((ntr, ntr), np.nan)),
+              "out_test": pin(np.full((nte, ntr), np.nan))}
+    K, Kx = compute_kernel_matrices(Xi, Ti, cfg, **kw)
+    ok = np.array_equal(K.entries, Kd) and np.array_equal(Kx.entries, Kxd)
+    cases += 1
+    entries += ntr * ntr + nte * ntr
+    if not ok:
+        print(f"MISMATCH n={n} L={L} ntr={ntr} nte={nte} pin_in={pin_in} pin_out={pin_out} "
+              f"fused={os.environ['QK_FUSED_BUILD']}", flush=True)
+        sys.exit(1)
+print(f"stress ok: {cases} cases, {entries / 1e9:.2f} G entries compared, "
+      f"{time.time() - t0:.0f} s", flush=True)
