@@ -36,11 +36,10 @@ struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
-  cudaStream_t h2d_stream = nullptr;  // chunked H2D feeding the in-kernel plane build
-  // angles, planes, K, progress, plane-block build states, chunk arrival marks
-  void* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  size_t cap[6] = {0, 0, 0, 0, 0, 0};
-  uint32_t epoch = 0;  // arrival marks hold the epoch of the call that wrote them
+  cudaStream_t h2d_stream = nullptr;  // the rest's upload + sweep of the head-first pipeline
+  // angles, planes, K, progress counters
+  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t cap[4] = {0, 0, 0, 0};
   uint64_t* bad = nullptr;  // [2]: non-finite sample sentinels (rows, cols)
   void* stage[2] = {nullptr, nullptr};  // pinned staging for pageable host buffers
   size_t stage_cap = 0;
@@ -75,29 +74,6 @@ struct Workspace {
                                             cudaGetErrorString(e));
     }
     cap[slot] = bytes;
-    return QK_OK;
-  }
-  // as ensure(), but a fresh allocation is zeroed (arrival marks: 0 is never an epoch)
-  qk_status ensure_zeroed(int slot, size_t bytes) {
-    const bool grow = cap[slot] < bytes;
-    if (qk_status s = ensure(slot, bytes)) return s;
-    if (grow && bytes) {
-      cudaError_t e = cudaMemsetAsync(buf[slot], 0, cap[slot], stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-      if (e != cudaSuccess)
-        return set_error(QK_ERR_CUDA, std::string("flag reset: ") + cudaGetErrorString(e));
-    }
-    return QK_OK;
-  }
-  // next call epoch for the arrival marks (0 is reserved for "never written")
-  qk_status next_epoch() {
-    if (++epoch == 0) {
-      epoch = 1;
-      cudaError_t e = cudaMemsetAsync(buf[5], 0, cap[5], stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-      if (e != cudaSuccess)
-        return set_error(QK_ERR_CUDA, std::string("flag reset: ") + cudaGetErrorString(e));
-    }
     return QK_OK;
   }
 };
@@ -381,130 +357,6 @@ StreamWaitValue32Fn stream_wait_value32() {
   return fn;
 }
 
-typedef int (*StreamWriteValue32Fn)(cudaStream_t, uintptr_t, uint32_t, unsigned int);
-
-StreamWriteValue32Fn stream_write_value32() {
-  static StreamWriteValue32Fn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess) {
-      cudaGetLastError();
-      return StreamWriteValue32Fn(nullptr);
-    }
-    return reinterpret_cast<StreamWriteValue32Fn>(p);
-  }();
-  return fn;
-}
-
-// In-kernel plane build for the host pipelines (opt-in, QK_FUSED_BUILD=1; L <= 2, pinned
-// angle buffers, stream memory operations available): the angles go up in chunks of
-// kArriveBlocks plane blocks on w->h2d_stream, each followed by an arrival mark, and the
-// sweep starts at once — its CTAs build each plane block as soon as its chunk has landed, so
-// the H2D of the inputs overlaps the sweep instead of preceding it.
-// Under a tool that serialises GPU work (ncu, compute-sanitizer) the sweep could not see
-// chunks land while it runs; there the chunks are copied first (QK_FUSED_PREARRIVE=1 forces
-// this), so the in-kernel build never waits.  The tools are recognised by their injection
-// environment or by their injection library in the process's mappings.
-bool fused_prearrive() {
-  static const bool on = [] {
-    const char* v = getenv("QK_FUSED_PREARRIVE");
-    if (v != nullptr) return v[0] == '1';
-    for (const char* e : {"CUDA_INJECTION64_PATH", "NVIDIA_PROCESS_INJECTION_XML_TARGET_SETTINGS",
-                          "NV_COMPUTE_PROFILER_PERFWORKS_DIR"})
-      if (getenv(e) != nullptr) return true;
-    FILE* f = fopen("/proc/self/maps", "r");
-    if (f == nullptr) return false;
-    char line[1024];
-    bool hit = false;
-    while (!hit && fgets(line, sizeof line, f) != nullptr)
-      hit = strstr(line, "TreeLauncherTargetInjection") != nullptr ||
-            strstr(line, "libsanitizer-collection") != nullptr;
-    fclose(f);
-    return hit;
-  }();
-  return on;
-}
-
-bool fused_build_enabled(const Plan& p) {
-  // opt-in (QK_FUSED_BUILD=1): on one B200 the fused sweep runs ~1.5 % below the plain one
-  // (ptxas schedules its loop with more dependency waits), which cancels the hidden H2D, so
-  // the default is the upload + gate-build path
-  const char* v = getenv("QK_FUSED_BUILD");
-  return v != nullptr && v[0] == '1' && p.layers <= 2 && stream_write_value32() != nullptr &&
-         stream_wait_value32() != nullptr;
-}
-
-// Sets up set `k` of `fb` for n samples: build states in w->buf[4] at element offset
-// state_off, arrival marks in w->buf[5] at offset arr_off.
-void fused_set(Workspace* w, FusedBuild& fb, int k, const Plan& p, double* dX, int64_t n,
-               void* planes, int64_t state_off, int64_t arr_off, unsigned long long* bad) {
-  PlaneSrc& s = fb.set[k];
-  s.X = dX;
-  s.n = n;
-  s.ld = p.width;
-  s.planes = planes;
-  s.state = static_cast<int*>(w->buf[4]) + state_off;
-  s.arrived = static_cast<unsigned int*>(w->buf[5]) + arr_off;
-  s.epoch = w->epoch;
-  s.bad = bad;
-}
-
-// Enqueues the chunked H2D of set `k` on w->h2d_stream, each chunk followed by its arrival
-// mark.  Called right AFTER the sweep launch: the sweep waits for the marks, never the
-// reverse, and the host's enqueue time then overlaps the sweep's start.
-qk_status fused_h2d(Workspace* w, const PlaneSrc& s, const double* hX) {
-  const int64_t nb = blocks_for(s.n), pad = sample_pad(s.n);
-  StreamWriteValue32Fn write = stream_write_value32();
-  double* dX = const_cast<double*>(s.X);
-  unsigned int* arr = const_cast<unsigned int*>(s.arrived);
-  cudaError_t err = cudaSuccess;
-  for (int64_t c = 0; c * kArriveBlocks < nb; ++c) {
-    const int64_t s0 = std::max<int64_t>(0, c * kArriveBlocks * kTile - pad);
-    const int64_t s1 = std::min<int64_t>(s.n, (c + 1) * kArriveBlocks * kTile - pad);
-    if (s1 > s0 && err == cudaSuccess)
-      err = cudaMemcpyAsync(dX + s0 * s.ld, hX + s0 * s.ld, size_t(s1 - s0) * s.ld * sizeof(double),
-                            cudaMemcpyHostToDevice, w->h2d_stream);
-    // marks go out even after a failed copy so the running sweep can finish
-    if (write(w->h2d_stream, reinterpret_cast<uintptr_t>(arr + c), s.epoch, 0) != 0)
-      return set_error(QK_ERR_CUDA, "cuStreamWriteValue32 failed");
-  }
-  return cuda_err(err, "H2D chunk");
-}
-
-int64_t arrive_chunks(int64_t n) { return (blocks_for(n) + kArriveBlocks - 1) / kArriveBlocks; }
-
-// Fused-build setup for up to two plane sets (set k: device angles dX[k], n[k] samples,
-// planes[k]); resets the build states and sentinels on w->stream.
-qk_status fused_setup(Workspace* w, const Plan& p, FusedBuild& fb, int n_sets, double* const* dX,
-                      const int64_t* n, void* const* planes) {
-  int64_t nb = 0, na = 0;
-  for (int k = 0; k < n_sets; ++k) {
-    nb += blocks_for(n[k]);
-    na += arrive_chunks(n[k]);
-  }
-  if (qk_status s = w->ensure(4, size_t(2 * nb + 2) * sizeof(int))) return s;  // + built counters
-  if (qk_status s = w->ensure_zeroed(5, size_t(std::max<int64_t>(na, 1)) * sizeof(unsigned)))
-    return s;
-  if (qk_status s = w->next_epoch()) return s;
-  if (cudaError_t e = cudaMemsetAsync(w->buf[4], 0, size_t(2 * nb + 2) * sizeof(int), w->stream))
-    return cuda_err(e, "build state reset");
-  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), w->stream))
-    return cuda_err(e, "sentinel reset");
-  int64_t so = 0, ao = 0;
-  for (int k = 0; k < n_sets; ++k) {
-    fused_set(w, fb, k, p, dX[k], n[k], planes[k], 2 * so, ao,
-              reinterpret_cast<unsigned long long*>(w->bad) + k);
-    fb.set[k].built = static_cast<int*>(w->buf[4]) + 2 * nb + k;
-    fb.set[k].nblocks = int(blocks_for(n[k]));
-    so += blocks_for(n[k]);
-    ao += arrive_chunks(n[k]);
-  }
-  if (n_sets == 1) fb.set[1] = fb.set[0];
-  return QK_OK;
-}
-
 // Head-first overlap of the input upload (pinned inputs, L = 2, the default host pipeline;
 // QK_HEAD_SPLIT=0 turns it off): the angles of the first B plane blocks go up and are
 // gate-built, the sweep runs the B x B Gram head (decode_gram orders it first) while the rest
@@ -566,8 +418,7 @@ struct Trace {
 
 template <class Launch>
 qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targets,
-                        Launch&& launch, Trace* trace = nullptr,
-                        const std::function<qk_status()>& after_launch = {}) {
+                        Launch&& launch, Trace* trace = nullptr) {
   StreamWaitValue32Fn wait = stream_wait_value32();
   int64_t n_rows_total = 0;  // one counter per tile row
   bool all_pinned = true;
@@ -601,27 +452,9 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   cudaEventCreateWithFlags(&reset, cudaEventDisableTiming);
   cudaEventRecord(reset, w->stream);
   if (trace) trace->mark(2, w->stream);
-  if (after_launch && fused_prearrive()) {  // feed the chunks first (serialising tools)
-    if (qk_status s = after_launch()) {
-      cudaEventDestroy(reset);
-      return s;
-    }
-    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) {
-      cudaEventDestroy(reset);
-      return cuda_err(e, "H2D chunks");
-    }
-  }
   if (qk_status s = launch()) {
     cudaEventDestroy(reset);
     return s;
-  }
-  if (after_launch && !fused_prearrive()) {
-    cudaStreamQuery(w->stream);  // the sweep is on its way; feed it
-    if (qk_status s = after_launch()) {
-      cudaStreamSynchronize(w->stream);  // a sweep waiting for missing chunks traps (20 s)
-      cudaEventDestroy(reset);
-      return s;
-    }
   }
   if (trace) trace->mark(3, w->stream);
   cudaStream_t cs = w->copy_stream;
@@ -785,37 +618,22 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   char* dPc = dPr + prb;
   cudaStream_t st = w->stream;
   Trace trace(st);
-  const bool fused = fused_build_enabled(*p) && is_pinned(h_rows) && is_pinned(h_cols);
-  FusedBuild fb;
-  if (fused) {
-    double* dXs[2] = {dXr, dXc};
-    const int64_t ns[2] = {n_rows, n_cols};
-    void* ps[2] = {dPr, dPc};
-    if (qk_status s = fused_setup(w, *p, fb, 2, dXs, ns, ps)) return s;
-    trace.mark(1, st);
-  } else {
-    if (qk_status s = upload(w, dXr, h_rows, xrb)) return s;
-    if (qk_status s = upload(w, dXc, h_cols, xcb)) return s;
-    trace.mark(1, st);
-    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
-      return cuda_err(e, "sentinel reset");
-    if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
-    if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st))
-      return s;
-  }
+  if (qk_status s = upload(w, dXr, h_rows, xrb)) return s;
+  if (qk_status s = upload(w, dXc, h_cols, xcb)) return s;
+  trace.mark(1, st);
+  if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+    return cuda_err(e, "sentinel reset");
+  if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
+  if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st))
+    return s;
   DrainTarget tg[1] = {
       {static_cast<double*>(w->buf[2]), h_K, n_rows, n_cols, kModeCross, nullptr}};
   if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
         return launch_sweep(*p, kModeCross, dPr, n_rows, dPc, n_cols, 0,
                             qk_cross_tile_count(plan, n_rows, n_cols), tg[0].d_K, n_cols,
-                            QK_OUT_DENSE, w->stream, tg[0].d_prog, fused ? &fb : nullptr);
-      }, &trace, fused ? std::function<qk_status()>([&]() -> qk_status {
-        if (qk_status s = fused_h2d(w, fb.set[1], h_cols)) return s;  // train (cols) first
-        return fused_h2d(w, fb.set[0], h_rows);
-      }) : std::function<qk_status()>()))
+                            QK_OUT_DENSE, w->stream, tg[0].d_prog);
+      }, &trace))
     return s;
-  if (fused)
-    if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
   static const char* const names[2] = {"test", "train"};
   return check_bad(w->bad, 2, names);
 }
@@ -849,21 +667,11 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
   double* dKs = dKt + size_t(n_train) * size_t(n_train);
   cudaStream_t st = w->stream;
   Trace trace(st);
-  const bool fused = fused_build_enabled(*p) && is_pinned(h_train) &&
-                     (n_test == 0 || is_pinned(h_test));
-  FusedBuild fb;
-  if (fused) {
-    double* dXs2[2] = {dXt, dXs};
-    const int64_t ns[2] = {n_train, n_test};
-    void* ps[2] = {dPt, dPs};
-    if (qk_status s = fused_setup(w, *p, fb, n_test > 0 ? 2 : 1, dXs2, ns, ps)) return s;
-    trace.mark(1, st);
-  }
   DrainTarget tg[2] = {{dKt, h_K_train, n_train, n_train, kModeGram, nullptr},
                        {dKs, h_K_cross, n_test, n_train, kModeCross, nullptr}};
   const int64_t nt = qk_job_tile_count(plan, n_train, n_test);
   const int n_targets = n_test > 0 ? 2 : 1;
-  const int64_t B = !fused && is_pinned(h_train) && (n_test == 0 || is_pinned(h_test))
+  const int64_t B = is_pinned(h_train) && (n_test == 0 || is_pinned(h_test))
                         ? choose_head(*p, n_train, n_test)
                         : 0;
   if (B > 0) {
@@ -895,17 +703,19 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
       cudaEvent_t* ev;
       ~Destroy() { cudaEventDestroy(ev[0]), cudaEventDestroy(ev[1]); }
     } destroy{ev};
-    if (cudaError_t e = cudaEventRecord(ev[0], st)) return cuda_err(e, "cudaEventRecord");
     if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&]() -> qk_status {
+          // ev[0] follows the head planes, the sentinel reset AND run_and_drain's progress
+          // counter reset, so the rest sweep's counter bumps are ordered after that reset
+          if (cudaError_t e = cudaEventRecord(ev[0], st)) return cuda_err(e, "cudaEventRecord");
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, 0, n_head, dKt, dKs, st,
-                                        tg[0].d_prog, tg[1].d_prog, nullptr, B))
+                                        tg[0].d_prog, tg[1].d_prog, B))
             return s2;
           cudaError_t e = cudaMemcpyAsync(dXt + s1 * p->width, h_train + s1 * p->width,
                                           size_t(n_train - s1) * row, cudaMemcpyHostToDevice,
                                           hs);
           if (e == cudaSuccess && n_test > 0)
             e = cudaMemcpyAsync(dXs, h_test, xsb, cudaMemcpyHostToDevice, hs);
-          if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev[0], 0);  // head planes, sentinel
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev[0], 0);  // head planes, resets
           // on a failure past this point, let the rest's queued work finish before returning
           // (it reads and writes the workspace the next call reuses)
           auto fail = [&](qk_status s2) {
@@ -918,7 +728,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
           if (qk_status s2 = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, hs))
             return fail(s2);
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, hs,
-                                        tg[0].d_prog, tg[1].d_prog, nullptr, B))
+                                        tg[0].d_prog, tg[1].d_prog, B))
             return fail(s2);
           e = cudaEventRecord(ev[1], hs);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[1], 0);
@@ -926,28 +736,19 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
         }, &trace))
       return s;
   } else {
-    if (!fused) {
-      if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
-      if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
-      trace.mark(1, st);
-      if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
-        return cuda_err(e, "sentinel reset");
-      if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
-      if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
-        return s;
-    }
+    if (qk_status s = upload(w, dXt, h_train, xtb)) return s;
+    if (qk_status s = upload(w, dXs, h_test, xsb)) return s;
+    trace.mark(1, st);
+    if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
+      return cuda_err(e, "sentinel reset");
+    if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
+    if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
+      return s;
     if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&] {
           return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
-                            tg[1].d_prog, fused ? &fb : nullptr);
-        }, &trace, fused ? std::function<qk_status()>([&]() -> qk_status {
-          if (qk_status s = fused_h2d(w, fb.set[0], h_train)) return s;
-          return n_test > 0 ? fused_h2d(w, fb.set[1], h_test) : QK_OK;
-        }) : std::function<qk_status()>()))
+                            tg[1].d_prog);
+        }, &trace))
       return s;
-    if (fused) {
-      print_fused_stats(148);
-      if (cudaError_t e = cudaStreamSynchronize(w->h2d_stream)) return cuda_err(e, "H2D chunks");
-    }
   }
   static const char* const names[2] = {"train", "test"};
   return check_bad(w->bad, 2, names);

@@ -26,24 +26,6 @@ constexpr int kGroup = 8;           // tile rows per super-row of the L2-friendl
 #endif
 constexpr int kRectGroup = QK_RECT_GROUP;  // tile rows per super-row of cross tile lists
 
-// In-kernel plane build (host pipelines with pinned inputs): angles arrive in chunks of
-// kArriveBlocks plane blocks; the copy stream marks each chunk with the call's epoch.
-constexpr int kArriveBlocks = 8;
-struct PlaneSrc {
-  const double* X = nullptr;           // device angles [n x width], filled during the launch
-  int64_t n = 0, ld = 0;
-  void* planes = nullptr;              // the plane set the sweep reads (double2 blocks)
-  int* state = nullptr;                // per block: [2b] slabs claimed, [2b+1] slabs built (zeroed)
-  int* built = nullptr;                // blocks built so far (zeroed); == nblocks: all done
-  int nblocks = 0;
-  const unsigned int* arrived = nullptr;  // per chunk: == epoch once its angles are copied
-  unsigned int epoch = 0;
-  unsigned long long* bad = nullptr;   // non-finite sentinel (atomicMin of the sample index)
-};
-struct FusedBuild {
-  PlaneSrc set[2];  // Gram/job: [0] train, [1] test; cross: [0] rows (test), [1] cols (train)
-};
-
 struct Plan {
   int32_t width = 0;
   int32_t layers = 0;
@@ -91,15 +73,13 @@ qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, in
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress = nullptr, const FusedBuild* fused = nullptr,
-                       int64_t head_b = 0);
+                       unsigned int* d_progress = nullptr, int64_t head_b = 0);
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
                         int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                         int64_t ld, void* stream);
 qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* d_b, int64_t n_b,
                        const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream);
 qk_status launch_dfma_peak(double* out, void* stream);
-void print_fused_stats(int grid);  // diagnostics (QK_FUSED_STATS=1)
 
 enum SweepMode { kModeGram = 0, kModeCross = 1, kModeJob = 2 };
 
@@ -108,8 +88,7 @@ enum SweepMode { kModeGram = 0, kModeCross = 1, kModeJob = 2 };
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train = nullptr,
-                     unsigned int* d_prog_cross = nullptr, const FusedBuild* fused = nullptr,
-                     int64_t head_b = 0);
+                     unsigned int* d_prog_cross = nullptr, int64_t head_b = 0);
 
 }  // namespace qk
 

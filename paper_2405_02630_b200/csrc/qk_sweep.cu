@@ -533,10 +533,7 @@ __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows,
 // ------------------------------------------------------------------------------------------
 // One 64-sample x 32-qubit slab of plane block `blk`: coalesced angle reads into a shared
 // transpose tile, then coalesced plane writes (qubit-major).  `tile` is 64 x 33 doubles.
-// Shared by the gate-build kernel and the sweep's in-kernel builder (bit-identical planes).
-// CG: read the angles through L2 only (the in-kernel builder reads angles that a copy engine
-// wrote during the same launch).
-template <bool CG, int QS>
+template <int QS>
 __device__ __forceinline__ void build_plane_slab(const double* __restrict__ X, int64_t n_samples,
                                                  int64_t ld, int width, int n_pad, int front,
                                                  int half, double2* __restrict__ planes,
@@ -549,7 +546,7 @@ __device__ __forceinline__ void build_plane_slab(const double* __restrict__ X, i
     const int q = q0 + qq - front;
     double x = 0.0;
     if (s >= 0 && s < n_samples && q >= 0 && q < width) {
-      x = CG ? __ldcg(X + s * ld + q) : __ldg(X + s * ld + q);
+      x = __ldg(X + s * ld + q);
       if (bad != nullptr && !isfinite(x)) atomicMin(bad, (unsigned long long)s);
     }
     tile[t][qq] = x;
@@ -572,7 +569,7 @@ __global__ void __launch_bounds__(256) gate_build_kernel(const double* __restric
                                                          int half, double2* __restrict__ planes,
                                                          unsigned long long* bad, int64_t blk0) {
   __shared__ double tile[kTile][33];
-  build_plane_slab<false, 32>(X, n_samples, ld, width, n_pad, front, half, planes, bad,
+  build_plane_slab<32>(X, n_samples, ld, width, n_pad, front, half, planes, bad,
                               blk0 + blockIdx.x, blockIdx.y * 32, tile);
 }
 
@@ -606,101 +603,10 @@ struct SweepArgs {
   double* out2;
   unsigned int* progress2;
   int pad_rows, pad_cols, pad_rows2;  // sample_pad() of each plane set (front of block 0)
-  // In-kernel plane build (fused = 1): the plane blocks of rows / cols / rows2 are built by
-  // the sweep's own CTAs from src[set_*] as their angles arrive (see ensure_block).
-  int fused, width, half;
-  int set_rows, set_cols, set_rows2;
-  PlaneSrc src[2];
-  unsigned long long* stats;  // diagnostics (QK_FUSED_STATS=1): per CTA ns in ensure, t0, t_end
   unsigned long long* next_tile;  // dynamic tile claims beyond the first wave (zeroed per launch)
   int64_t n_split;  // the last n_split tiles run as two row halves each (finer last wave)
   int64_t head_b;   // Gram tile order with a B-block head (decode_gram; 0: decode_upper)
 };
-
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void add_release_gpu(int* p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ int add_acq_rel_gpu(int* p, int v) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
-               : "memory");
-  return old;
-}
-
-// CTA-wide (every thread calls it; it ends on a barrier): make plane block b of `ps` exist.
-// A block is built in 64-qubit slabs that any CTA needing the block claims one at a time
-// (state[2b]: slabs claimed, state[2b+1]: slabs built), so the CTAs that reach a new block
-// together build it together.  Building needs the block's angles: the host stream writes the
-// call's epoch into arrived[b / kArriveBlocks] after each chunk of the H2D.  With `wait` the
-// CTA waits for the angles and then for the block to be complete; without (look-ahead: the
-// block is needed a tile later) it only claims slabs of a block whose angles have landed and
-// never waits.  A CTA never waits while holding an unbuilt claim, so this cannot deadlock;
-// a 20 s guard traps instead of hanging if an arrival never comes.
-__device__ __noinline__ void ensure_block(const PlaneSrc ps, int64_t b, int n_pad, int front,
-                                          int width, int half, double (*tile)[64 + 1], int* flag,
-                                          bool wait, unsigned long long* build_ns) {
-  const int nslabs = (n_pad + 63) / 64;
-  int* claimed = ps.state + 2 * b;
-  int* done = claimed + 1;
-  for (;;) {
-    if (threadIdx.x == 0) {
-      int slab = -1;
-      if (ld_acquire_gpu(done) < nslabs) {
-        const unsigned long long t0 = global_ns();
-        const unsigned int* arr = ps.arrived + b / kArriveBlocks;
-        bool ready = ld_acquire_sys(arr) == ps.epoch;
-        while (wait && !ready) {
-          __nanosleep(256);
-          if (global_ns() - t0 > 20000000000ull) __trap();
-          ready = ld_acquire_sys(arr) == ps.epoch;
-        }
-        if (ready && *(volatile int*)claimed < nslabs) {
-          const int k = atomicAdd(claimed, 1);
-          if (k < nslabs) slab = k;
-        }
-        if (slab < 0 && wait) {
-          while (ld_acquire_gpu(done) < nslabs) {
-            __nanosleep(256);
-            if (global_ns() - t0 > 20000000000ull) __trap();
-          }
-        }
-      }
-      *flag = slab;
-    }
-    __syncthreads();
-    const int slab = *flag;
-    if (slab < 0) break;
-    const unsigned long long tb = build_ns ? global_ns() : 0;
-    build_plane_slab<true, 64>(ps.X, ps.n, ps.ld, width, n_pad, front, half,
-                               static_cast<double2*>(ps.planes), ps.bad, b, slab * 64, tile);
-    __threadfence();
-    __syncthreads();  // the slab is written; the transpose tile and `flag` are free
-    if (threadIdx.x == 0) {
-      if (add_acq_rel_gpu(done, 1) == nslabs - 1) add_release_gpu(ps.built, 1);
-      if (build_ns) build_ns[0] += global_ns() - tb, build_ns[1] += 1;
-    }
-  }
-  __syncthreads();  // `flag` is reused by the next call
-}
 
 // Per-tile coordinates: tile rows/cols in plane blocks and which problem of a kModeJob launch.
 struct TileXY {
@@ -716,65 +622,7 @@ struct Claim {
   int half;   // -1: whole tile; 0 / 1: tile rows 0-31 / 32-63 only
 };
 
-// Shared-memory state of the fused plane build of one CTA.
-struct FusedState {
-  int ensured;      // CTA-local tile number up to which the planes are known to exist
-  int set_done[2];  // this CTA has seen every block of plane set s built (and fenced)
-  int build_flag;
-  unsigned long long stat[5];  // QK_FUSED_STATS: ensure ns, t0, first tile, build ns, builds
-};
-
-// Fused plane build, CTA-wide, out of line (keeps the sweep's registers for the sweep): make
-// the plane blocks of this CTA's tiles (ensured, last] exist, waiting for them; with
-// `lookahead` also build (never wait for) those of tile last + 1.  Once this CTA has seen
-// every block of a set built (one acquire of the set's counter, then one proxy fence), tiles
-// of that set need no check, barrier or fence.  `a` is a local copy of the kernel arguments.
-__device__ __noinline__ void fused_ensure(const SweepArgs* a, const Claim* ring, int64_t n_items,
-                                          int64_t last, bool lookahead, FusedState* fs,
-                                          double* stage_T) {
-  auto valid = [&](int64_t k) { return ring[k & 7].g < n_items; };
-  while (last > fs->ensured && !valid(last)) --last;  // claims past the end of the list
-  bool need = false;
-  for (int64_t k = fs->ensured + 1; k <= last; ++k) {
-    const Claim& c = ring[k & 7];
-    need |= !fs->set_done[c.prob ? a->set_rows2 : a->set_rows] || !fs->set_done[a->set_cols];
-  }
-  if (!need) {
-    // every thread computed the same `last` and stores the same value: a thread that reads
-    // the new value scans an empty range and reaches the same (no-op) outcome
-    if (last > fs->ensured) fs->ensured = int(last);
-    return;
-  }
-  __syncthreads();  // every warp is past the previous epilogue (stage_T is the build tile)
-  const unsigned long long e0 = a->stats ? global_ns() : 0;
-  unsigned long long* bst = a->stats ? fs->stat + 3 : nullptr;
-  double (*tile)[65] = reinterpret_cast<double (*)[65]>(stage_T);
-  auto blocks = [&](const Claim& c, bool wait) {
-    const int si = c.prob ? a->set_rows2 : a->set_rows;
-    if (!fs->set_done[si])
-      ensure_block(a->src[si], c.bi, a->n_pad, a->front, a->width, a->half, tile,
-                   &fs->build_flag, wait, bst);
-    if (!fs->set_done[a->set_cols])
-      ensure_block(a->src[a->set_cols], c.bj, a->n_pad, a->front, a->width, a->half, tile,
-                   &fs->build_flag, wait, bst);
-  };
-  for (int64_t k = fs->ensured + 1; k <= last; ++k) blocks(ring[k & 7], true);
-  if (lookahead && valid(last + 1)) blocks(ring[(last + 1) & 7], false);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fs->ensured = int(last);
-    for (int s = 0; s < 2; ++s)
-      if (!fs->set_done[s] && ld_acquire_gpu(a->src[s].built) == a->src[s].nblocks)
-        fs->set_done[s] = 1;
-    if (a->stats) fs->stat[0] += global_ns() - e0;
-  }
-  // the planes were written through the generic proxy; the bulk copies read them through
-  // the async proxy
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  __syncthreads();  // ensured, set_done
-}
-
-template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
+template <int LAYERS, int MODE, int OUT, int RI>
 __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   using St = typename BondT<LAYERS>::type;
   constexpr int kRI = Geo<RI>::kRI, kWarps = Geo<RI>::kWarps;
@@ -794,9 +642,6 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   // (thread 0) at the start of tile k and published by a CTA barrier.  Claims live in a small
   // shared ring indexed by the CTA-local tile number.
   const int kLook = 1 + (kStages - 1) / nchunks;
-  // the fused plane build also looks one tile further ahead (it builds, never waits for, the
-  // blocks of tile k + kLook + 1), so that tile is claimed too
-  const int kClaim = kLook + (FUSED ? 1 : 0);
   __shared__ Claim ring[8];
   double* stage_T = reinterpret_cast<double*>(released + 2 * kStages);  // epilogue staging tile
   // Work items: tiles [0, n_tiles - n_split) whole, then the last n_split tiles as two row
@@ -836,18 +681,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
     return TileXY{c.bi, c.bj, c.prob};
   };
   if (tid == 0)
-    for (int64_t k = 0; k <= kClaim; ++k) claim(k);
+    for (int64_t k = 0; k <= kLook; ++k) claim(k);
   __syncthreads();
-  // fused plane build state (shared memory) and a local copy of the arguments for it
-  __shared__ FusedState fs;
-  if (FUSED && tid == 0) {
-    fs.ensured = -1;
-    fs.set_done[0] = fs.set_done[1] = 0;
-    for (int q = 0; q < 5; ++q) fs.stat[q] = 0;
-    if (a.stats) fs.stat[1] = global_ns();
-  }
-  if (FUSED) __syncthreads();
-  if constexpr (FUSED) fused_ensure(&a, ring, n_items, (kStages - 1) / nchunks, false, &fs, stage_T);
   auto issue = [&](int64_t f) {  // fill stage f % kStages with item f (if its tile exists)
     const int64_t k = f / nchunks;
     if (!valid(k)) return;
@@ -881,15 +716,9 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   St st[kRI][kRJ];
   int64_t f = 0;
   for (int64_t k = 0; valid(k); ++k) {
-    if (k > 0) {  // claim tile k + kClaim (the chunks of tile k + kLook are issued during tile k)
-      if (tid == 0) claim(k + kClaim);
+    if (k > 0) {  // claim tile k + kLook (its chunks are issued during tile k)
+      if (tid == 0) claim(k + kLook);
       __syncthreads();
-    }
-    // fused build: the blocks of tile k + 1 are needed once its first chunks are issued
-    // (during tile k); ensure them here, where no bond state is live
-    if constexpr (FUSED) {
-      fused_ensure(&a, ring, n_items, k + 1 + (kStages - 1) / nchunks, true, &fs, stage_T);
-      if (k == 0 && a.stats && tid == 0) fs.stat[2] = global_ns();
     }
     const TileXY tk = tile_of(k);
     // padding rows of this tile (front of plane block 0): warps made only of them skip the
@@ -1055,32 +884,11 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       if (tid == 0) atomicAdd(prog + bi, half < 0 ? 2u : 1u);  // per tile row: 2 per tile
     }
   }
-  if constexpr (FUSED) {
-    if (a.stats != nullptr && tid == 0) {
-      a.stats[6 * blockIdx.x] = fs.stat[0];
-      a.stats[6 * blockIdx.x + 1] = fs.stat[1];
-      a.stats[6 * blockIdx.x + 2] = global_ns();
-      a.stats[6 * blockIdx.x + 3] = fs.stat[3];
-      a.stats[6 * blockIdx.x + 4] = fs.stat[4];
-      a.stats[6 * blockIdx.x + 5] = fs.stat[2];
-    }
-  }
 }
 
-template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
-__global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
-  sweep_body<LAYERS, MODE, OUT, RI, false>(a);
-}
-
-// The in-kernel plane build adds an out-of-line call per tile; capping the registers at the
-// plain kernel's count keeps ptxas from re-allocating the sweep loop around it.
-#ifndef QK_FUSED_MAXNREG
-#define QK_FUSED_MAXNREG 120
-#endif
 template <int LAYERS, int MODE, int OUT, int RI>
-__global__ void __maxnreg__(QK_FUSED_MAXNREG)
-    sweep_kernel_fused(const SweepArgs a) {
-  sweep_body<LAYERS, MODE, OUT, RI, true>(a);
+__global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
+  sweep_body<LAYERS, MODE, OUT, RI>(a);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1489,11 +1297,10 @@ static qk_status tile_counter(cudaStream_t st, unsigned long long** out) {
                      "tile counter reset");
 }
 
-template <int LAYERS, int MODE, int OUT, int RI, bool FUSED>
+template <int LAYERS, int MODE, int OUT, int RI>
 static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
   if (qk_status s = tile_counter(st, &a.next_tile)) return s;
-  auto kern = FUSED ? sweep_kernel_fused<LAYERS, MODE, OUT, RI>
-                    : sweep_kernel<LAYERS, MODE, OUT, RI, false>;
+  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI>;
   constexpr int threads = Geo<RI>::kThreads;
   // per call: the attribute is per device and costs microseconds
   cudaError_t e =
@@ -1507,11 +1314,11 @@ static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
   int64_t grid = int64_t(sms) * per_sm;
   // the last wave runs as half tiles (QK_EPI == 1 epilogue: whole tiles only)
-  static const int split_mode = [] {  // QK_HALF_TILES: 0 off, 1 on, 2 plain kernel only
+  static const int split_mode = [] {  // QK_HALF_TILES: 0 off, 1 on
     const char* v = getenv("QK_HALF_TILES");
     return v == nullptr ? 1 : v[0] - '0';
   }();
-  const bool split = QK_EPI != 1 && (split_mode == 1 || (split_mode == 2 && !FUSED));
+  const bool split = QK_EPI != 1 && split_mode == 1;
   a.n_split = split ? std::min<int64_t>(a.n_tiles, grid) : 0;
   if (grid > a.n_tiles + a.n_split) grid = a.n_tiles + a.n_split;
   kern<<<unsigned(grid), threads, kSmemBytes, st>>>(a);
@@ -1533,14 +1340,8 @@ static int sweep_ri(int layers) {
 
 template <int LAYERS, int MODE, int OUT>
 static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
-  if constexpr (OUT == QK_OUT_DENSE) {  // the in-kernel plane build serves the host pipelines
-    if (a.fused) {
-      if (sweep_ri(LAYERS) == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, true>(a, st);
-      return launch_sweep_ri<LAYERS, MODE, OUT, 4, true>(a, st);
-    }
-  }
-  if (sweep_ri(LAYERS) == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2, false>(a, st);
-  return launch_sweep_ri<LAYERS, MODE, OUT, 4, false>(a, st);
+  if (sweep_ri(LAYERS) == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2>(a, st);
+  return launch_sweep_ri<LAYERS, MODE, OUT, 4>(a, st);
 }
 
 template <int LAYERS, int MODE, int OUT>
@@ -1599,69 +1400,15 @@ static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, 
   return cuda_status(cudaGetLastError(), "deep pairs launch");
 }
 
-// QK_FUSED_STATS=1 (diagnostics): per-CTA time spent building / waiting for plane blocks,
-// printed after each fused launch.
-static unsigned long long* fused_stats() {
-  static unsigned long long* buf = [] {
-    const char* v = getenv("QK_FUSED_STATS");
-    unsigned long long* b = nullptr;
-    if (v != nullptr && v[0] == '1' && cudaMallocManaged(&b, 6 * 4096 * 8) != cudaSuccess) b = nullptr;
-    return b;
-  }();
-  return buf;
-}
-
-void print_fused_stats(int grid) {
-  unsigned long long* s = fused_stats();
-  if (s == nullptr) return;
-  cudaDeviceSynchronize();
-  unsigned long long t0 = ~0ull, t1 = 0, mx = 0, sum = 0, bsum = 0, bn = 0, bmx = 0, fmx = 0;
-  unsigned long long first_end = ~0ull;
-  for (int b = 0; b < grid; ++b) t0 = std::min(t0, s[6 * b + 1]);
-  for (int b = 0; b < grid; ++b) {
-    t1 = std::max(t1, s[6 * b + 2]);
-    first_end = std::min(first_end, s[6 * b + 2]);
-    mx = std::max(mx, s[6 * b]);
-    sum += s[6 * b];
-    bsum += s[6 * b + 3];
-    bn += s[6 * b + 4];
-    bmx = std::max(bmx, s[6 * b + 3]);
-    fmx = std::max(fmx, s[6 * b + 5] - t0);
-  }
-  fprintf(stderr,
-          "qk_fused_stats kernel %.3f ms, ensure max %.3f mean %.3f ms, builds %llu (%.1f us "
-          "each, max per CTA %.3f ms), first tile by %.3f ms, CTA ends %.3f..%.3f ms\n",
-          (t1 - t0) * 1e-6, mx * 1e-6, sum * 1e-6 / grid, bn, bn ? bsum * 1e-3 / bn : 0.0,
-          bmx * 1e-6, fmx * 1e-6, (first_end - t0) * 1e-6, (t1 - t0) * 1e-6);
-}
-
-static void set_fused(SweepArgs& a, const Plan& p, const FusedBuild* fb, int rows, int cols,
-                      int rows2) {
-  if (fb == nullptr || p.layers > 2) return;  // L >= 3 kernels read prebuilt planes
-  a.stats = fused_stats();
-  a.fused = 1;
-  a.width = p.width;
-  a.half = p.layers == 2 ? 0 : 1;
-  a.src[0] = fb->set[0];
-  a.src[1] = fb->set[1];
-  a.set_rows = rows;
-  a.set_cols = cols;
-  a.set_rows2 = rows2;
-}
-
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress, const FusedBuild* fused, int64_t head_b) {
+                       unsigned int* d_progress, int64_t head_b) {
   if (tile_end <= tile_begin) return QK_OK;
-  if (fused != nullptr && p.layers > 2)
-    return set_error(QK_ERR_VALUE, "in-kernel plane build needs layers <= 2");
   if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
     return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
   SweepArgs a{};
   if (mode == kModeGram) a.head_b = head_b;
-  if (mode == kModeGram) set_fused(a, p, fused, 0, 0, 0);
-  else set_fused(a, p, fused, 0, 1, 0);
   a.progress = d_progress;
   a.rows = static_cast<const double2*>(d_rows);
   a.cols = static_cast<const double2*>(d_cols);
@@ -1720,35 +1467,24 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train,
-                     unsigned int* d_prog_cross, const FusedBuild* fused, int64_t head_b) {
+                     unsigned int* d_prog_cross, int64_t head_b) {
   if (tile_end <= tile_begin) return QK_OK;
-  if (fused != nullptr && p.layers > 2)
-    return set_error(QK_ERR_VALUE, "in-kernel plane build needs layers <= 2");
   if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
     return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
   const int64_t nbt = blocks_for(n_train);
   const int64_t n_gram = nbt * (nbt + 1) / 2;
   if (p.layers >= 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
     // one problem only (or the one-pair-per-thread L >= 3 kernel): plain launches
-    FusedBuild gram_fb, cross_fb;
-    if (fused != nullptr) {
-      gram_fb.set[0] = gram_fb.set[1] = fused->set[0];
-      cross_fb.set[0] = fused->set[1];  // cross: [0] rows (test), [1] cols (train)
-      cross_fb.set[1] = fused->set[0];
-    }
     if (qk_status s = launch_sweep(p, kModeGram, d_train, n_train, d_train, n_train, tile_begin,
                                    std::min(tile_end, n_gram), d_K_train, n_train,
-                                   QK_OUT_DENSE, stream, d_prog_train,
-                                   fused ? &gram_fb : nullptr, head_b))
+                                   QK_OUT_DENSE, stream, d_prog_train, head_b))
       return s;
     if (n_test == 0 || tile_end <= n_gram) return QK_OK;
     return launch_sweep(p, kModeCross, d_test, n_test, d_train, n_train,
                         std::max(tile_begin, n_gram) - n_gram, tile_end - n_gram, d_K_cross,
-                        n_train, QK_OUT_DENSE, stream, d_prog_cross,
-                        fused ? &cross_fb : nullptr);
+                        n_train, QK_OUT_DENSE, stream, d_prog_cross);
   }
   SweepArgs a{};
-  set_fused(a, p, fused, 0, 0, 1);
   a.head_b = head_b;
   a.rows = static_cast<const double2*>(d_train);
   a.cols = static_cast<const double2*>(d_train);

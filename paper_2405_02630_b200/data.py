@@ -57,8 +57,13 @@ def _silhouette_prototype(rng: np.random.Generator, ink: float = 0.5) -> np.ndar
     return np.clip(mask * tex, 0.0, 1.0)
 
 
-def synthetic_images(n: int, kind: str = "mnist", seed: int = 0, classes: int = 10):
-    """(images [n, 784] in [0, 1], labels [n]) — balanced over `classes`."""
+def synthetic_images(n: int, kind: str = "mnist", seed: int = 0, classes: int = 10,
+                     mix: float = 0.0):
+    """(images [n, 784] in [0, 1], labels [n]) — balanced over `classes`.
+
+    ``mix`` > 0 makes the classes overlap: sample k blends its class prototype with the
+    prototype of another random class, weight m ~ U(0, mix) on the other one (m > 0.5 looks
+    more like the other class), so a classifier cannot reach accuracy 1 (parity runs)."""
     rng = np.random.default_rng(seed)
     make = _stroke_prototype if kind == "mnist" else _silhouette_prototype
     protos = np.stack([make(rng) for _ in range(classes)])
@@ -66,8 +71,14 @@ def synthetic_images(n: int, kind: str = "mnist", seed: int = 0, classes: int = 
     rng.shuffle(labels)
     X = np.empty((n, PIXELS))
     shifts = rng.integers(-2, 3, size=(n, 2))
+    if mix > 0:
+        other = (labels + rng.integers(1, classes, n)) % classes
+        weight = rng.uniform(0.0, mix, n)
     for k in range(n):
-        img = np.roll(protos[labels[k]], tuple(shifts[k]), axis=(0, 1))
+        base = protos[labels[k]]
+        if mix > 0:
+            base = (1.0 - weight[k]) * base + weight[k] * protos[other[k]]
+        img = np.roll(base, tuple(shifts[k]), axis=(0, 1))
         ink = img > 0
         noise = rng.normal(0.0, 0.1, img.shape) * ink
         if kind != "mnist":
@@ -109,15 +120,15 @@ def pixel_angles(images: np.ndarray, bw: float = 1.0) -> np.ndarray:
 
 def config_data(config_id: int, n_train: int, n_test: int, kind: str = "mnist",
                 features: int | None = None, bw: float = 1.0, binary: tuple | None = None,
-                classes: int = 10):
+                classes: int = 10, mix: float = 0.0):
     """Angles for one config: seed = 240502630 + config_id."""
     seed = 240502630 + config_id
     if binary is not None:
-        X, y = synthetic_images(4 * (n_train + n_test), kind, seed, classes)
+        X, y = synthetic_images(4 * (n_train + n_test), kind, seed, classes, mix)
         keep = np.isin(y, binary)
         X, y = X[keep][: n_train + n_test], y[keep][: n_train + n_test]
     else:
-        X, y = synthetic_images(n_train + n_test, kind, seed, classes)
+        X, y = synthetic_images(n_train + n_test, kind, seed, classes, mix)
     Xtr, ytr, Xte, yte = X[:n_train], y[:n_train], X[n_train:], y[n_train:]
     if features is not None:
         mu, comps = pca_fit(Xtr, features)

@@ -1,6 +1,6 @@
 """Host-pipeline phase timing (QK_TRACE=1 prints h2d / gate / sweep / tail / host per call):
 config 4 (10,000 x 784 train, 2,000 test) through compute_kernel_matrices with pinned
-buffers.  usage: QK_TRACE=1 [QK_FUSED_BUILD=1] [QK_HEAD_SPLIT=0] python tools/e2e_trace.py [calls]"""
+buffers.  usage: QK_TRACE=1 [QK_HEAD_SPLIT=0] python tools/e2e_trace.py [calls]"""
 import sys
 import time
 from pathlib import Path

@@ -1,5 +1,5 @@
 """Randomised stress of the host pipelines (head-first two-stream overlap, per-tile-row
-drains, pinned / pageable inputs and outputs, in-kernel build on/off) against the
+drains, pinned / pageable inputs and outputs) against the
 device-resident path, bit for bit.  usage: python tools/stress_pipelines.py [seconds]"""
 import os
 import sys
@@ -34,7 +34,6 @@ while time.time() - t0 < budget:
                                       torch.as_tensor(T, device="cuda"), cfg)
     Kd, Kxd = Kd.entries.cpu().numpy(), Kxd.entries.cpu().numpy()
     pin_in, pin_out = bool(rng.integers(2)), bool(rng.integers(2))
-    os.environ["QK_FUSED_BUILD"] = "1" if rng.integers(4) == 0 else "0"
     Xi, Ti = (pin(X), pin(T)) if pin_in else (X, T)
     kw = {}
     if pin_out:
@@ -45,8 +44,8 @@ while time.time() - t0 < budget:
     cases += 1
     entries += ntr * ntr + nte * ntr
     if not ok:
-        print(f"MISMATCH n={n} L={L} ntr={ntr} nte={nte} pin_in={pin_in} pin_out={pin_out} "
-              f"fused={os.environ['QK_FUSED_BUILD']}", flush=True)
+        print(f"MISMATCH n={n} L={L} ntr={ntr} nte={nte} pin_in={pin_in} pin_out={pin_out}",
+              flush=True)
         sys.exit(1)
 print(f"stress ok: {cases} cases, {entries / 1e9:.2f} G entries compared, "
       f"{time.time() - t0:.0f} s", flush=True)
