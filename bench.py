@@ -4,8 +4,8 @@ Workload (BASELINE.json configs[3], the config the 1/2/4/8-GPU metric is quoted 
 GPU): MNIST-shaped synthetic data, 784 qubits, L = 2, train Gram 10000 x 10000 (49,995,000
 strict-upper entries; diagonal injected) + test-versus-train cross 2000 x 10000 (20,000,000
 entries).  One step = gate build + pair sweeps of the whole job; for N > 1 the tile list is
-split into equal contiguous ranges and every rank's sweep stores its tiles straight into rank
-0's matrices over NVLink (CUDA IPC), closed by one barrier (distributed.py).
+split into contiguous ranges of equal estimated cost and every rank's sweep stores its tiles
+straight into rank 0's matrices over NVLink (CUDA IPC), closed by one barrier (distributed.py).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -13,8 +13,11 @@ split into equal contiguous ranges and every rank's sweep stores its tiles strai
 value       whole-job entries/s, device-resident inputs, CUDA events, max over ranks
 e2e         same metric through the public API with host (pinned) buffers, H2D + D2H inside
 roofline    sweep kernel, executed FP64 flops / CUDA-event launch time vs B200 FP64 peak
-cpu_baseline  oracle/ (the reference's contraction restated in C) on the host cores, sampled
---impl reference  that CPU baseline as the reference arm (rank 0 only)
+cpu_baseline  oracle/ (the reference's contraction restated in C) on the host cores, sampled;
+            plus .reference_python: the unmodified reference package (baseline/_ref) itself,
+            contract_batch(workers=os.cpu_count()) on 512 sampled pairs in a CUDA-free
+            subprocess, with its amplitudes compared against this run's matrices
+--impl reference  the oracle CPU baseline as the reference arm (rank 0 only)
 """
 from __future__ import annotations
 
@@ -90,24 +93,10 @@ def cpu_baseline_run(Atr, Ate, seconds: float, seed: int = 0):
 
     threads = host_threads()
     rng = np.random.default_rng(seed)
-    n_gram = N_TRAIN * (N_TRAIN - 1) // 2
-    total = n_gram + N_TEST * N_TRAIN
     A = np.concatenate([Atr, Ate])
 
     def sample(P):
-        # uniform over the job's pair set: Gram strict-upper pairs + cross pairs
-        out = np.empty((P, 2), dtype=np.int64)
-        for k in range(P):
-            while True:
-                if rng.integers(total) < n_gram:
-                    i, j = rng.integers(N_TRAIN, size=2)
-                    if i < j:
-                        out[k] = (i, j)
-                        break
-                else:
-                    out[k] = (N_TRAIN + rng.integers(N_TEST), rng.integers(N_TRAIN))
-                    break
-        return out
+        return sample_pairs(rng, P)
 
     cal = sample(max(threads * 2, 8))
     t0 = time.perf_counter()
@@ -123,6 +112,56 @@ def cpu_baseline_run(Atr, Ate, seconds: float, seed: int = 0):
                       f"(seed {seed}); oracle/qk_oracle.c complex128 TN contraction, "
                       f"{threads} pthreads on {cpu_model()}",
             "seconds": dt}
+
+
+def sample_pairs(rng, P):
+    """P pairs uniform over the workload's pair set (Gram strict upper + cross), as row
+    indices into concat(train, test)."""
+    n_gram = N_TRAIN * (N_TRAIN - 1) // 2
+    total = n_gram + N_TEST * N_TRAIN
+    out = np.empty((P, 2), dtype=np.int64)
+    for k in range(P):
+        while True:
+            if rng.integers(total) < n_gram:
+                i, j = rng.integers(N_TRAIN, size=2)
+                if i < j:
+                    out[k] = (i, j)
+                    break
+            else:
+                out[k] = (N_TRAIN + rng.integers(N_TEST), rng.integers(N_TRAIN))
+                break
+    return out
+
+
+def reference_python_run(Atr, Ate, n_pairs: int = 512, repeats: int = 3, seed: int = 7):
+    """The unmodified reference (baseline/_ref) timed on the host cores: contract_batch over
+    n_pairs sampled pairs with workers=os.cpu_count(), median of `repeats`, planning timed
+    separately, in a subprocess that sees no CUDA device.  Returns the record
+    and (pairs, amplitudes) for a parity check."""
+    import tempfile
+
+    script = ROOT / "tools" / "ref_baseline.py"
+    if not (ROOT / "baseline" / "_ref" / "tnkernel").is_dir():
+        return {"unavailable": "baseline/_ref (pip install --target of the reference) absent"}, None
+    pairs = sample_pairs(np.random.default_rng(seed), n_pairs)
+    with tempfile.TemporaryDirectory() as td:
+        a, p, o = Path(td) / "a.npy", Path(td) / "p.npy", Path(td) / "o.json"
+        np.save(a, np.concatenate([Atr, Ate]))
+        np.save(p, pairs)
+        env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+        try:
+            subprocess.run([sys.executable, str(script), str(a), str(p), str(o), str(repeats)],
+                           env=env, check=True, timeout=900, capture_output=True)
+            r = json.loads(o.read_text())
+        except (subprocess.SubprocessError, OSError, ValueError) as exc:
+            return {"unavailable": f"reference run failed: {str(exc)[:200]}"}, None
+    rec = {"value": r["entries_per_s"], "unit": UNIT, "cores": r["workers"], "kind": "reference",
+           "sample": f"{len(pairs)} pairs sampled uniformly from the workload (seed {seed}); "
+                     "unmodified reference tnkernel.engine.contract_batch(simplified kernel "
+                     f"network, plan_contraction path, workers={r['workers']}) on "
+                     f"{cpu_model()}, median of {repeats}",
+           "plan_s": r["plan_s"], "runs_s": r["runs_s"]}
+    return rec, (pairs, np.asarray(r["amplitudes_re"]))
 
 
 def run_reference(args):
@@ -223,6 +262,12 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"[bench] rank {rank}/{world}: backend {dist.get_backend()}"
+              f"{' nccl ' + '.'.join(map(str, torch.cuda.nccl.version())) if not shared_gpu else ''}"
+              f", cuda:{local} {torch.cuda.get_device_name(local)} "
+              f"bus {getattr(torch.cuda.get_device_properties(local), 'pci_bus_id', '?')}",
+              file=sys.stderr,
+              flush=True)
     from paper_2405_02630_b200 import FeatureMapConfig, compute_kernel_matrices, plan_for
     from paper_2405_02630_b200 import device as qdev
     from paper_2405_02630_b200.distributed import KernelJob
@@ -280,7 +325,7 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(args.steps):
-        job.run(tr, te)
+        K_last = job.run(tr, te)
     t1.record()
     torch.cuda.synchronize()
     recording[0] = False
@@ -300,7 +345,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (the pair sweep), per rank, from live CUDA events
     n_sweep = len(sweep_events)
-    my_entries = entries / world
+    my_entries = job.layout.rank_entries(rank)  # this rank's cost-balanced tile range
     flops_exec = my_entries * info["flops_per_entry"] * args.steps
     achieved_tf = flops_exec / sweep_s / 1e12 if sweep_s > 0 else None
     props = torch.cuda.get_device_properties(local)
@@ -333,7 +378,10 @@ def run_ours(args):
                              "MEASURED_PEAKS.json); peak_measured_dfma = qk_dfma_peak "
                              "microbenchmark in this run",
                 "sweep_share_of_step": sweep_s / elapsed if elapsed > 0 else None,
-                "sweep_launches": n_sweep}
+                "sweep_launches": n_sweep, "rank_entries_per_step": my_entries}
+    if world > 1 and roofline["frac"] is not None:
+        roofline["frac_min_over_ranks"] = allreduce_scalar(roofline["frac"], dist.ReduceOp.MIN)
+        roofline["frac_max_over_ranks"] = allreduce_scalar(roofline["frac"], dist.ReduceOp.MAX)
 
     # e2e through the public API with pinned host buffers (N = 1: the C-ABI host pipeline;
     # N > 1: per-rank H2D + sharded job + gather + D2H on rank 0)
@@ -376,10 +424,39 @@ def run_ours(args):
                                   "over NVLink, each rank drains its row slice to shared host "
                                   "memory over its own PCIe link)"}
 
+    # the default public call: pageable numpy in, pageable numpy out (N = 1)
+    e2e_pageable = None
+    if args.e2e_steps > 0 and world == 1:
+        compute_kernel_matrices(Atr, Ate, cfg)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(max(1, args.e2e_steps - 1)):
+            compute_kernel_matrices(Atr, Ate, cfg)
+        e_el = (time.perf_counter() - w0) / max(1, args.e2e_steps - 1)
+        e2e_pageable = {"value": entries / e_el, "unit": UNIT, "ms_per_step": 1e3 * e_el,
+                        "steps": max(1, args.e2e_steps - 1),
+                        "h2d_bytes_per_step": int(Atr.nbytes + Ate.nbytes),
+                        "d2h_bytes_per_step": int(8 * (N_TRAIN * N_TRAIN + N_TEST * N_TRAIN)),
+                        "api": "compute_kernel_matrices(train, test, cfg): pageable numpy in "
+                               "and out (fresh output arrays every call)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_run(Atr, Ate, args.cpu_seconds)
         cpu.pop("seconds", None)
+        ref, got = reference_python_run(Atr, Ate)
+        if got is not None:
+            pairs, amp = got
+            K, Kx = (k.cpu().numpy() for k in K_last)
+            ours = np.where(pairs[:, 0] < N_TRAIN, K[np.minimum(pairs[:, 0], N_TRAIN - 1),
+                                                     pairs[:, 1]],
+                            Kx[np.maximum(pairs[:, 0] - N_TRAIN, 0), pairs[:, 1]])
+            ref["parity_vs_this_run"] = {
+                "pairs": int(len(pairs)),
+                "max_abs_dK": float(np.abs(ours - amp * amp).max()),
+                "max_rel_d_amplitude": float(np.max(np.abs(np.sqrt(ours) - np.abs(amp)) /
+                                                    np.maximum(np.abs(amp), 1e-300)))}
+        cpu["reference_python"] = ref
 
     launches_total = launches_per_step * args.steps
     if world > 1:
@@ -391,7 +468,8 @@ def run_ours(args):
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": dict(WORKLOAD, parallelism=f"tile-sharded x{world}",
                               entries_per_step=entries),
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "e2e_pageable": e2e_pageable, "clocks": clk,
                "gpu_launches": int(launches_total),
                "gpu": props.name, "plan": info}
         print(json.dumps(out), flush=True)

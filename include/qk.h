@@ -172,6 +172,13 @@ qk_status qk_shared_free(void* d_ptr);
 qk_status qk_ipc_export(const void* d_ptr, unsigned char out_handle[QK_IPC_HANDLE_BYTES]);
 qk_status qk_ipc_import(const unsigned char handle[QK_IPC_HANDLE_BYTES], void** out_d_ptr);
 qk_status qk_ipc_close(void* d_ptr);
+/* Placement decision before any import: the PCI bus id of the current device (so ranks whose
+ * processes see different device orderings can name it), and whether the current device can
+ * store into memory of the device with that bus id (1: the same device, or peer access over
+ * NVLink / PCIe; 0: not visible to this process, or no peer access -> gather placement). */
+#define QK_BUS_ID_BYTES 32
+qk_status qk_device_bus_id(char out_bus_id[QK_BUS_ID_BYTES]);
+qk_status qk_can_reach(const char* bus_id, int32_t* out_reachable);
 /* Host side of the multi-GPU result: a row-major host matrix that every rank process maps
  * (a POSIX shared-memory segment) is page-locked in each of them (qk_host_register), and
  * each rank copies ITS row slice of rank 0's device matrix into it (qk_copy_d2h: a

@@ -72,6 +72,8 @@ _SIGNATURES = {
     "qk_ipc_export": (ctypes.c_int, [_c_vp, ctypes.c_char_p]),
     "qk_ipc_import": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_c_vp)]),
     "qk_ipc_close": (ctypes.c_int, [_c_vp]),
+    "qk_device_bus_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "qk_can_reach": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32)]),
     "qk_host_register": (ctypes.c_int, [_c_vp, _c_sz]),
     "qk_host_unregister": (ctypes.c_int, [_c_vp]),
     "qk_copy_d2h": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),

@@ -623,8 +623,8 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   trace.mark(1, st);
   if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
     return cuda_err(e, "sentinel reset");
-  if (qk_status s = launch_gate_build(*p, dXr, n_rows, p->width, dPr, w->bad, st)) return s;
-  if (qk_status s = launch_gate_build(*p, dXc, n_cols, p->width, dPc, w->bad + 1, st))
+  if (qk_status s = launch_gate_build2(*p, dXr, n_rows, dPr, w->bad, dXc, n_cols, dPc,
+                                       w->bad + 1, st))
     return s;
   DrainTarget tg[1] = {
       {static_cast<double*>(w->buf[2]), h_K, n_rows, n_cols, kModeCross, nullptr}};
@@ -723,9 +723,8 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
             return s2;
           };
           if (e != cudaSuccess) return fail(cuda_err(e, "H2D rest"));
-          if (qk_status s2 = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, hs, B))
-            return fail(s2);
-          if (qk_status s2 = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, hs))
+          if (qk_status s2 = launch_gate_build2(*p, dXt, n_train, dPt, w->bad, dXs, n_test, dPs,
+                                                w->bad + 1, hs, B))
             return fail(s2);
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, hs,
                                         tg[0].d_prog, tg[1].d_prog, B))
@@ -741,8 +740,8 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
     trace.mark(1, st);
     if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
       return cuda_err(e, "sentinel reset");
-    if (qk_status s = launch_gate_build(*p, dXt, n_train, p->width, dPt, w->bad, st)) return s;
-    if (qk_status s = launch_gate_build(*p, dXs, n_test, p->width, dPs, w->bad + 1, st))
+    if (qk_status s = launch_gate_build2(*p, dXt, n_train, dPt, w->bad, dXs, n_test, dPs,
+                                         w->bad + 1, st))
       return s;
     if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&] {
           return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
@@ -814,6 +813,32 @@ qk_status qk_ipc_import(const unsigned char handle[QK_IPC_HANDLE_BYTES], void** 
   *out_d_ptr = nullptr;
   return cuda_err(cudaIpcOpenMemHandle(out_d_ptr, h, cudaIpcMemLazyEnablePeerAccess),
                   "cudaIpcOpenMemHandle");
+}
+
+qk_status qk_device_bus_id(char out_bus_id[QK_BUS_ID_BYTES]) {
+  if (out_bus_id == nullptr) return set_error(QK_ERR_VALUE, "NULL output");
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_err(e, "cudaGetDevice");
+  return cuda_err(cudaDeviceGetPCIBusId(out_bus_id, QK_BUS_ID_BYTES, dev), "cudaDeviceGetPCIBusId");
+}
+
+qk_status qk_can_reach(const char* bus_id, int32_t* out_reachable) {
+  if (bus_id == nullptr || out_reachable == nullptr) return set_error(QK_ERR_VALUE, "NULL argument");
+  *out_reachable = 0;
+  int dev = 0, peer = -1;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_err(e, "cudaGetDevice");
+  if (cudaDeviceGetByPCIBusId(&peer, bus_id) != cudaSuccess) {
+    cudaGetLastError();  // the owner's device is not visible to this process
+    return QK_OK;
+  }
+  if (peer == dev) {
+    *out_reachable = 1;
+    return QK_OK;
+  }
+  int ok = 0;
+  if (cudaError_t e = cudaDeviceCanAccessPeer(&ok, dev, peer)) return cuda_err(e, "cudaDeviceCanAccessPeer");
+  *out_reachable = ok ? 1 : 0;
+  return QK_OK;
 }
 
 qk_status qk_ipc_close(void* d_ptr) {

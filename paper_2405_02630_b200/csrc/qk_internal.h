@@ -70,6 +70,11 @@ QK_HD inline int64_t upper_row_offset(int64_t r, int64_t nb) { return r * nb - r
 qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
                             void* d_planes, uint64_t* d_bad, void* stream,
                             int64_t blk_begin = 0, int64_t blk_end = -1);
+// Two plane sets (train and test, width-long rows) in ONE launch; set a from block blk_begin_a.
+qk_status launch_gate_build2(const Plan& p, const double* d_a, int64_t n_a, void* d_planes_a,
+                             uint64_t* d_bad_a, const double* d_b, int64_t n_b,
+                             void* d_planes_b, uint64_t* d_bad_b, void* stream,
+                             int64_t blk_begin_a = 0);
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,

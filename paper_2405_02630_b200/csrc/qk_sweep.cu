@@ -24,7 +24,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 
@@ -531,46 +533,78 @@ __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows,
 // ------------------------------------------------------------------------------------------
 // Gate build: angles -> planes[block][q][t] = (cos x, sin x)  (L = 2)  or  half angles (L != 2)
 // ------------------------------------------------------------------------------------------
-// One 64-sample x 32-qubit slab of plane block `blk`: coalesced angle reads into a shared
-// transpose tile, then coalesced plane writes (qubit-major).  `tile` is 64 x 33 doubles.
-template <int QS>
-__device__ __forceinline__ void build_plane_slab(const double* __restrict__ X, int64_t n_samples,
-                                                 int64_t ld, int width, int n_pad, int front,
-                                                 int half, double2* __restrict__ planes,
-                                                 unsigned long long* bad, int64_t blk, int q0,
-                                                 double (*tile)[QS + 1]) {
-  const int spad = sample_pad(n_samples);
-  for (int idx = threadIdx.x; idx < kTile * QS; idx += blockDim.x) {
-    const int t = idx / QS, qq = idx % QS;
-    const int64_t s = blk * kTile + t - spad;  // padding slots (s < 0) get angle 0
-    const int q = q0 + qq - front;
-    double x = 0.0;
-    if (s >= 0 && s < n_samples && q >= 0 && q < width) {
-      x = __ldg(X + s * ld + q);
-      if (bad != nullptr && !isfinite(x)) atomicMin(bad, (unsigned long long)s);
-    }
-    tile[t][qq] = x;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < kTile * QS; idx += blockDim.x) {
-    const int qq = idx >> 6, t = idx & 63;
-    const int q = q0 + qq;
-    if (q >= n_pad) break;
-    const double x = tile[t][qq];
-    double sn, cs;
-    sincos(half ? 0.5 * x : x, &sn, &cs);
-    planes[(blk * n_pad + q) * kTile + t] = make_double2(cs, sn);
-  }
-}
+// One plane set of a launch: angles X [n x ld] (sample-major), plane blocks [blk0, blk0 + nblk).
+struct GateSet {
+  const double* X;
+  int64_t n, ld;
+  double2* planes;
+  unsigned long long* bad;  // optional: atomicMin of the first non-finite sample
+  int64_t blk0, nblk;
+};
 
-__global__ void __launch_bounds__(256) gate_build_kernel(const double* __restrict__ X,
-                                                         int64_t n_samples, int64_t ld,
-                                                         int width, int n_pad, int front,
-                                                         int half, double2* __restrict__ planes,
-                                                         unsigned long long* bad, int64_t blk0) {
-  __shared__ double tile[kTile][33];
-  build_plane_slab<32>(X, n_samples, ld, width, n_pad, front, half, planes, bad,
-                              blk0 + blockIdx.x, blockIdx.y * 32, tile);
+// One CTA = one plane block (64 samples) x 64 plane qubits.  Thread (t = tid % 64,
+// u = tid / 64) owns sample t and the qubit quads u, u + 4, u + 8, u + 12 of the slab: it
+// issues all of its angle loads first — VEC: each quad is one 32-byte sector of the sample's
+// row (two 16 B loads), so every fetched sector is used whole — then computes the 16
+// (cos, sin) pairs and stores them, a warp writing 32 consecutive samples of one qubit (512
+// contiguous bytes).  No shared memory, no barrier: the loads of the next quads overlap the
+// sincos of the previous ones.  Padding samples (front of block 0) and the identity qubits of
+// the width padding (front of the chain) get angle 0.  A second plane set (e.g. the test
+// samples of a joint job) rides in the same launch: blockIdx.x >= s0.nblk selects it.
+constexpr int kGateQuads = 4;                       // quads per thread
+constexpr int kGateQubits = 4 * 4 * kGateQuads;     // 64 plane qubits per CTA
+template <bool VEC>
+__global__ void __launch_bounds__(256) gate_build_kernel(GateSet s0, GateSet s1, int width,
+                                                         int n_pad, int front, int half) {
+  const bool second = blockIdx.x >= s0.nblk;
+  const GateSet& gs = second ? s1 : s0;
+  const int64_t blk = gs.blk0 + (second ? blockIdx.x - s0.nblk : blockIdx.x);
+  const int t = threadIdx.x & 63, u = threadIdx.x >> 6;
+  const int64_t s = blk * kTile + t - sample_pad(gs.n);
+  const bool live = s >= 0 && s < gs.n;
+  const double* row = gs.X + (live ? s : 0) * gs.ld;
+  const int q_slab = blockIdx.y * kGateQubits;
+  double x[kGateQuads][4];
+#pragma unroll
+  for (int k = 0; k < kGateQuads; ++k) {
+    const int q0 = q_slab + 4 * (u + 4 * k);  // plane qubit of element 0 of the quad
+    const int qi = q0 - front;                // its input qubit
+    if (VEC) {
+      // front % 4 == 0 and n_pad % 4 == 0: a quad is wholly input qubits or wholly padding
+      if (live && qi >= 0 && qi < width) {
+        const double2 lo = __ldg(reinterpret_cast<const double2*>(row + qi));
+        const double2 hi = __ldg(reinterpret_cast<const double2*>(row + qi) + 1);
+        x[k][0] = lo.x, x[k][1] = lo.y, x[k][2] = hi.x, x[k][3] = hi.y;
+      } else {
+        x[k][0] = x[k][1] = x[k][2] = x[k][3] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        x[k][e] = live && qi + e >= 0 && qi + e < width ? __ldg(row + qi + e) : 0.0;
+    }
+  }
+  if (gs.bad != nullptr) {
+    bool finite = true;
+#pragma unroll
+    for (int k = 0; k < kGateQuads; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) finite = finite && isfinite(x[k][e]);
+    if (!finite) atomicMin(gs.bad, (unsigned long long)s);  // padding values are 0: live
+  }
+  double2* out = gs.planes + blk * int64_t(n_pad) * kTile + t;
+#pragma unroll
+  for (int k = 0; k < kGateQuads; ++k) {
+    const int q0 = q_slab + 4 * (u + 4 * k);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (q0 + e < n_pad) {
+        double sn, cs;
+        sincos(half ? 0.5 * x[k][e] : x[k][e], &sn, &cs);
+        out[int64_t(q0 + e) * kTile] = make_double2(cs, sn);
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1257,59 +1291,136 @@ static qk_status cuda_status(cudaError_t e, const char* what) {
 }
 
 static int sm_count() {
+  static std::atomic<int> cache[64];
   int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  if ((sms = cache[dev].load(std::memory_order_relaxed)) > 0) return sms;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  cache[dev].store(sms, std::memory_order_relaxed);
   return sms;
+}
+
+// Resident CTAs per SM of a kernel with `smem` bytes of dynamic shared memory, after opting it
+// in to that much shared memory — once per (kernel, device): the attribute call and the
+// occupancy query cost microseconds of host time, which small jobs notice.
+template <class Kern>
+static qk_status resident_ctas(Kern kern, int threads, size_t smem, int* per_sm) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_status(e, "cudaGetDevice");
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), dev, threads, smem);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *per_sm = it->second;
+    return QK_OK;
+  }
+  if (smem > 48 * 1024)
+    if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem)))
+      return cuda_status(e, "smem attribute");
+  int n = 0;
+  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem))
+    return cuda_status(e, "occupancy");
+  *per_sm = n < 1 ? 1 : n;
+  cache.emplace(key, *per_sm);
+  return QK_OK;
+}
+
+// Plane sets s0 (and s1 when s1.nblk > 0) in one launch.
+static qk_status launch_gate_sets(const Plan& p, GateSet s0, GateSet s1, cudaStream_t st) {
+  const int64_t nb = s0.nblk + s1.nblk;
+  if (nb <= 0) return QK_OK;
+  auto al32 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 31u) == 0; };
+  const bool vec = p.front_pad % 4 == 0 && s0.ld % 4 == 0 && al32(s0.X) &&
+                   (s1.nblk == 0 || (s1.ld % 4 == 0 && al32(s1.X)));
+  dim3 grid(unsigned(nb), unsigned((p.width_padded + kGateQubits - 1) / kGateQubits));
+  const int half = p.layers == 2 ? 0 : 1;
+  if (vec)
+    gate_build_kernel<true><<<grid, 256, 0, st>>>(s0, s1, p.width, p.width_padded, p.front_pad,
+                                                  half);
+  else
+    gate_build_kernel<false><<<grid, 256, 0, st>>>(s0, s1, p.width, p.width_padded,
+                                                   p.front_pad, half);
+  return cuda_status(cudaGetLastError(), "gate_build launch");
+}
+
+static GateSet gate_set(const double* X, int64_t n, int64_t ld, void* planes, uint64_t* bad,
+                        int64_t blk_begin, int64_t blk_end) {
+  if (blk_end < 0 || blk_end > blocks_for(n)) blk_end = blocks_for(n);
+  GateSet g{X, n, ld, static_cast<double2*>(planes),
+            reinterpret_cast<unsigned long long*>(bad), blk_begin,
+            n == 0 ? 0 : std::max<int64_t>(0, blk_end - blk_begin)};
+  return g;
 }
 
 qk_status launch_gate_build(const Plan& p, const double* d_angles, int64_t n, int64_t ld,
                             void* d_planes, uint64_t* d_bad, void* stream, int64_t blk_begin,
                             int64_t blk_end) {
   if (n == 0) return QK_OK;
-  if (blk_end < 0 || blk_end > blocks_for(n)) blk_end = blocks_for(n);
-  if (blk_end <= blk_begin) return QK_OK;
-  dim3 grid(unsigned(blk_end - blk_begin), unsigned((p.width_padded + 31) / 32));
-  gate_build_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      d_angles, n, ld, p.width, p.width_padded, p.front_pad, p.layers == 2 ? 0 : 1,
-      static_cast<double2*>(d_planes), reinterpret_cast<unsigned long long*>(d_bad), blk_begin);
-  return cuda_status(cudaGetLastError(), "gate_build launch");
+  return launch_gate_sets(p, gate_set(d_angles, n, ld, d_planes, d_bad, blk_begin, blk_end),
+                          GateSet{}, static_cast<cudaStream_t>(stream));
+}
+
+qk_status launch_gate_build2(const Plan& p, const double* d_a, int64_t n_a, void* d_planes_a,
+                             uint64_t* d_bad_a, const double* d_b, int64_t n_b,
+                             void* d_planes_b, uint64_t* d_bad_b, void* stream,
+                             int64_t blk_begin_a) {
+  return launch_gate_sets(p, gate_set(d_a, n_a, p.width, d_planes_a, d_bad_a, blk_begin_a, -1),
+                          gate_set(d_b, n_b, p.width, d_planes_b, d_bad_b, 0, -1),
+                          static_cast<cudaStream_t>(stream));
 }
 
 // Per-launch tile-claim counters (the dynamic schedule): a ring of zeroed 8-byte slots per
-// device, one per launch, so concurrent launches on different streams never share one.
-static qk_status tile_counter(cudaStream_t st, unsigned long long** out) {
+// device, one per launch, so concurrent launches on different streams never share one.  A
+// launch captured into a CUDA graph gets its own stream-ordered allocation instead (a graph
+// memory node, allocated and freed around the kernel on every replay), so a replay never
+// shares a counter with a later ring launch.  *owned: the caller frees it after the launch.
+static qk_status tile_counter(cudaStream_t st, unsigned long long** out, bool* owned) {
   constexpr int kSlots = 4096;
   static unsigned long long* pool[64] = {};
   static std::mutex mu;
   static std::atomic<uint64_t> seq{0};
-  int dev = 0;
-  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_status(e, "cudaGetDevice");
-  if (dev < 0 || dev >= 64) return set_error(QK_ERR_CUDA, "device index out of range");
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (pool[dev] == nullptr)
-      if (cudaError_t e = cudaMalloc(&pool[dev], kSlots * sizeof(unsigned long long)))
-        return cuda_status(e, "tile counter allocation");
+  *owned = false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaError_t e = cudaStreamIsCapturing(st, &cap)) return cuda_status(e, "capture query");
+  if (cap == cudaStreamCaptureStatusActive) {
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), sizeof(unsigned long long), st))
+      return cuda_status(e, "captured tile counter");
+    *owned = true;
+  } else {
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return cuda_status(e, "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return set_error(QK_ERR_CUDA, "device index out of range");
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (pool[dev] == nullptr)
+        if (cudaError_t e = cudaMalloc(&pool[dev], kSlots * sizeof(unsigned long long)))
+          return cuda_status(e, "tile counter allocation");
+    }
+    *out = pool[dev] + (seq.fetch_add(1) % kSlots);
   }
-  *out = pool[dev] + (seq.fetch_add(1) % kSlots);
   return cuda_status(cudaMemsetAsync(*out, 0, sizeof(unsigned long long), st),
                      "tile counter reset");
 }
 
 template <int LAYERS, int MODE, int OUT, int RI>
 static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
-  if (qk_status s = tile_counter(st, &a.next_tile)) return s;
+  bool owned = false;
+  if (qk_status s = tile_counter(st, &a.next_tile, &owned)) return s;
+  struct Release {  // a captured counter is freed after the launch, on the same stream
+    unsigned long long* p;
+    cudaStream_t st;
+    bool on;
+    ~Release() {
+      if (on) cudaFreeAsync(p, st);
+    }
+  } release{a.next_tile, st, owned};
   auto kern = sweep_kernel<LAYERS, MODE, OUT, RI>;
   constexpr int threads = Geo<RI>::kThreads;
-  // per call: the attribute is per device and costs microseconds
-  cudaError_t e =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
-  if (e != cudaSuccess) return cuda_status(e, "sweep smem attribute");
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, kSmemBytes);
-  if (e != cudaSuccess) return cuda_status(e, "sweep occupancy");
-  if (per_sm < 1) per_sm = 1;
+  if (qk_status s = resident_ctas(kern, threads, kSmemBytes, &per_sm)) return s;
   const int sms = sm_count();
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
   int64_t grid = int64_t(sms) * per_sm;
@@ -1348,11 +1459,10 @@ template <int LAYERS, int MODE, int OUT>
 static qk_status launch_general(const SweepArgs& a, cudaStream_t st) {
   auto kern = sweep_general_kernel<LAYERS, MODE, OUT>;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-  if (e != cudaSuccess) return cuda_status(e, "general sweep occupancy");
+  if (qk_status s = resident_ctas(kern, 256, 0, &per_sm)) return s;
   const int sms = sm_count();
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
-  int64_t grid = int64_t(sms) * (per_sm < 1 ? 1 : per_sm);
+  int64_t grid = int64_t(sms) * per_sm;
   if (grid > a.n_tiles * 16) grid = a.n_tiles * 16;
   kern<<<unsigned(grid), 256, 0, st>>>(a);
   return cuda_status(cudaGetLastError(), "general sweep launch");
@@ -1362,14 +1472,11 @@ template <int M, int MODE, int OUT>
 static qk_status launch_deep(const SweepArgs& a, cudaStream_t st) {
   auto kern = sweep_deep_kernel<M, MODE, OUT>;
   constexpr size_t smem = Deep<M>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return cuda_status(e, "deep sweep smem attribute");
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDeepThreads, smem);
-  if (e != cudaSuccess) return cuda_status(e, "deep sweep occupancy");
+  if (qk_status s = resident_ctas(kern, kDeepThreads, smem, &per_sm)) return s;
   const int sms = sm_count();
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
-  int64_t grid = int64_t(sms) * (per_sm < 1 ? 1 : per_sm);
+  int64_t grid = int64_t(sms) * per_sm;
   const int64_t items = a.n_tiles * Deep<M>::kGroups;
   if (grid > items) grid = items;
   kern<<<unsigned(grid), kDeepThreads, smem, st>>>(a);
@@ -1391,8 +1498,8 @@ static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, 
                                    double* d_amp, cudaStream_t st) {
   auto kern = pairs_deep_kernel<M>;
   constexpr size_t smem = Deep<M>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return cuda_status(e, "deep pairs smem attribute");
+  int per_sm = 0;
+  if (qk_status s = resident_ctas(kern, kDeepThreads, smem, &per_sm)) return s;
   const int64_t grid = (n_pairs + Deep<M>::PP - 1) / Deep<M>::PP;
   kern<<<unsigned(grid), kDeepThreads, smem, st>>>(
       static_cast<const double2*>(d_a), n_a, static_cast<const double2*>(d_b), n_b, d_pairs,

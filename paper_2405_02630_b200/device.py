@@ -21,10 +21,20 @@ def _stream() -> int:
 def _require(t: torch.Tensor, name: str, dtype=None) -> None:
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise DeviceError(f"{name} must be a CUDA tensor (the engine has no CPU path)")
+    _on_current(t, name)
     if dtype is not None and t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+
+
+def _on_current(t: torch.Tensor, name: str) -> None:
+    """Launches go to torch's current stream on the current device: a tensor on another GPU
+    would be read by the wrong device's kernels, so it is refused (torch.cuda.set_device or
+    ``with torch.cuda.device(...)`` selects the device)."""
+    cur = torch.cuda.current_device()
+    if t.device.index != cur:
+        raise DeviceError(f"{name} is on {t.device} but the current device is cuda:{cur}")
 
 
 def angles_to_device(x, device=None) -> torch.Tensor:
@@ -76,6 +86,7 @@ def gram(planes: Planes, out: torch.Tensor | None = None, tile_begin: int = 0,
     Dense: writes an N x N fp64 matrix (strict upper computed, mirrored, unit diagonal).
     Packed: returns the tile-major buffer of the range (edge^2 doubles per tile)."""
     plan, n = planes.plan, planes.n
+    _on_current(planes.buf, "planes")
     nt = plan.gram_tile_count(n)
     tile_end = nt if tile_end is None else tile_end
     edge = plan.tile_edge
@@ -93,6 +104,8 @@ def cross(rows: Planes, cols: Planes, out: torch.Tensor | None = None, tile_begi
           tile_end: int | None = None, packed: bool = False) -> torch.Tensor:
     """Test-versus-train block K[r][c] over rectangle tiles [tile_begin, tile_end)."""
     plan = rows.plan
+    _on_current(rows.buf, "row planes")
+    _on_current(cols.buf, "column planes")
     nt = plan.cross_tile_count(rows.n, cols.n)
     tile_end = nt if tile_end is None else tile_end
     edge = plan.tile_edge
@@ -111,6 +124,7 @@ def cross(rows: Planes, cols: Planes, out: torch.Tensor | None = None, tile_begi
 def gram_into(planes: Planes, out_ptr: int, tile_begin: int, tile_end: int) -> None:
     """Dense Gram tiles [tile_begin, tile_end) stored at a raw device address (e.g. a peer
     rank's matrix imported over CUDA IPC; row-major N x N)."""
+    _on_current(planes.buf, "planes")
     _native.check(_native.lib().qk_gram_tiles(planes.plan.handle, planes.ptr(), planes.n,
                                               tile_begin, tile_end, out_ptr,
                                               _native.QK_OUT_DENSE, _stream()))
@@ -118,6 +132,8 @@ def gram_into(planes: Planes, out_ptr: int, tile_begin: int, tile_end: int) -> N
 
 def cross_into(rows: Planes, cols: Planes, out_ptr: int, tile_begin: int, tile_end: int) -> None:
     """Dense cross tiles stored at a raw device address (row-major n_rows x n_cols)."""
+    _on_current(rows.buf, "row planes")
+    _on_current(cols.buf, "column planes")
     _native.check(_native.lib().qk_cross_tiles(rows.plan.handle, rows.ptr(), rows.n, cols.ptr(),
                                                cols.n, tile_begin, tile_end, out_ptr, cols.n,
                                                _native.QK_OUT_DENSE, _stream()))
@@ -128,6 +144,9 @@ def job_into(train: Planes, test: Planes | None, K_train_ptr: int, K_cross_ptr: 
     """Train Gram + test x train block as one tile list, one persistent launch, dense outputs
     at raw device addresses (row-major N_train x N_train and N_test x N_train)."""
     plan = train.plan
+    _on_current(train.buf, "train planes")
+    if test is not None:
+        _on_current(test.buf, "test planes")
     n_test = test.n if test is not None else 0
     nt = int(_native.lib().qk_job_tile_count(plan.handle, train.n, n_test))
     tile_end = nt if tile_end is None else tile_end
@@ -159,6 +178,8 @@ def unpack_cross(plan: SweepPlan, packed: torch.Tensor, n_rows: int, n_cols: int
 def pair_amplitudes(a: Planes, b: Planes, pairs: torch.Tensor) -> torch.Tensor:
     """Signed real amplitudes for explicit (p, q) index pairs, input order (engine.py:132)."""
     _require(pairs, "pairs", torch.int64)
+    _on_current(a.buf, "planes")
+    _on_current(b.buf, "planes")
     pairs = pairs.reshape(-1, 2).contiguous()
     out = torch.empty(pairs.shape[0], dtype=torch.float64, device=a.buf.device)
     _native.check(_native.lib().qk_pair_amplitudes(a.plan.handle, a.ptr(), a.n, b.ptr(), b.n,

@@ -3,9 +3,9 @@
 The reference parallelises over pairs only — a fork pool in code (engine.py:159-166),
 shard-run-then-merge in SPEC, MPI + NCCL across A100s in the paper
 (PAPER.md:359-362).  Here the unit is the sweep tile: the job's linearised tile list (train
-Gram upper-triangle tiles, then test x train cross tiles) is split into contiguous equal
-ranges (SPEC's contiguous ceil(P/W) rule at tile granularity; every tile costs the same, so
-equal counts are balanced).  Each rank builds the gate planes of every sample (cheap) and
+Gram upper-triangle tiles, then test x train cross tiles) is split into contiguous ranges of
+equal estimated cost (SPEC's contiguous ceil(P/W) rule at tile granularity; tile_costs).  Each
+rank builds the gate planes of every sample (cheap) and
 sweeps its range.  Two ways to land the results on rank 0:
 
 * ``placement="p2p"`` (default): rank 0 allocates the dense matrices and exports them over
@@ -37,8 +37,40 @@ import torch
 import torch.distributed as dist
 
 from . import _native
+from .errors import RebindError
 from .kernel_pipeline import shard_range
 from .planner import SweepPlan
+
+
+def _log(msg: str) -> None:
+    import sys
+
+    print(f"[qk] {msg}", file=sys.stderr, flush=True)
+
+
+def device_bus_id() -> str:
+    """PCI bus id of the current device (names it across processes with different orderings)."""
+    _native.bind_current_device()
+    buf = ctypes.create_string_buffer(32)
+    _native.check(_native.lib().qk_device_bus_id(buf))
+    return buf.value.decode()
+
+
+def can_reach(bus_id: str) -> bool:
+    """Whether this process's current device can store into the device with ``bus_id``."""
+    _native.bind_current_device()
+    out = ctypes.c_int32(0)
+    _native.check(_native.lib().qk_can_reach(bus_id.encode(), ctypes.byref(out)))
+    return bool(out.value)
+
+
+def agree_placement(reachable: bool, group=None) -> bool:
+    """All ranks agree on the p2p placement only if every rank can reach rank 0's memory
+    (one MIN all-reduce; a gloo group reduces on the CPU)."""
+    flag = torch.tensor([1.0 if reachable else 0.0], dtype=torch.float64,
+                        device="cpu" if dist.get_backend(group) == "gloo" else "cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item() >= 1.0)
 
 
 @dataclass(frozen=True)
@@ -92,6 +124,12 @@ class JobLayout:
         """Kernel entries the job defines: strict-upper Gram + full cross (the metric unit)."""
         return self.n_train * (self.n_train - 1) // 2 + self.n_test * self.n_train
 
+    def rank_entries(self, rank: int) -> int:
+        """Entries inside this rank's tile range (its share of the metric)."""
+        lo, hi = self.union_range(rank)
+        edge = int(round(self.tile_elems ** 0.5))
+        return int(tile_entries(self.n_train, self.n_test, edge)[lo:hi].sum())
+
 
 def _pad(n: int, edge: int) -> int:
     return (edge - n % edge) % edge
@@ -117,6 +155,40 @@ def tile_costs(n_train: int, n_test: int, edge: int, group: int = 8) -> np.ndarr
         g0 = nb * (nb + 1) // 2
         w[g0:g0 + nb] = row0_weight(n_test)  # cross tile row 0 (test block 0)
     return w
+
+
+def gram_tile_coords(nb: int, group: int = 8) -> tuple[np.ndarray, np.ndarray]:
+    """(bi, bj) of every Gram tile in the sweep kernel's list order (qk_sweep.cu decode_upper:
+    super-rows of `group` tile rows, each walked column by column)."""
+    bis, bjs = [], []
+    for r0 in range(0, nb, group):
+        h = min(group, nb - r0)
+        for c in range(h):  # the super-row's triangle: column r0 + c holds rows r0..r0+c
+            bis.append(np.arange(r0, r0 + c + 1))
+            bjs.append(np.full(c + 1, r0 + c))
+        cols = np.arange(r0 + h, nb)  # then full columns of h rows
+        bis.append(np.tile(np.arange(r0, r0 + h), len(cols)))
+        bjs.append(np.repeat(cols, h))
+    if not bis:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64)
+    return np.concatenate(bis).astype(np.int64), np.concatenate(bjs).astype(np.int64)
+
+
+def tile_entries(n_train: int, n_test: int, edge: int) -> np.ndarray:
+    """Kernel entries (the metric unit: strict-upper Gram pairs, cross pairs) inside every
+    tile of the joint list, in list order — for per-rank accounting of cost-balanced ranges."""
+    def real(n):  # real samples per plane block (the ragged remainder fills block 0's end)
+        nb = -(-n // edge) if n else 0
+        r = np.full(nb, edge, dtype=np.int64)
+        if nb:
+            r[0] = edge - _pad(n, edge)
+        return r
+    rt = real(n_train)
+    bi, bj = gram_tile_coords(len(rt))
+    gram = np.where(bi == bj, rt[bi] * (rt[bi] - 1) // 2, rt[bi] * rt[bj])
+    rs = real(n_test)
+    cross = np.outer(rs, rt).ravel()  # row-major tile list (kRectGroup = 1)
+    return np.concatenate([gram, cross])
 
 
 def layout_for(plan: SweepPlan, n_train: int, n_test: int, world: int) -> JobLayout:
@@ -320,36 +392,39 @@ class KernelJob:
 
     # ---- p2p placement: sweeps store into rank 0's matrices ----------------------------
     def _setup_shared(self):
+        """Collective: rank 0 allocates and exports the matrices with its device's PCI bus id;
+        every other rank checks it can store into that device (qk_can_reach: the same device,
+        or peer access) and imports the handles.  All ranks then agree on the placement: any
+        rank without a path to rank 0's memory sends everyone to the gather placement.  A
+        failing import on a rank that CAN reach rank 0 is a bug and is raised, not hidden."""
         lay = self.layout
         if self.rank == 0:
             mats = [SharedMatrix(lay.n_train, lay.n_train)]
             if lay.n_test:
                 mats.append(SharedMatrix(lay.n_test, lay.n_train))
-            handles = [m.export() for m in mats]
+            payload = ([m.export() for m in mats], device_bus_id())
         else:
-            mats, handles = None, None
-        box = [handles]
+            mats, payload = [], None
+        box = [payload]
         dist.broadcast_object_list(box, src=0, group=self.group)
-        ok = 1.0
-        if self.rank != 0:
+        handles, owner_bus = box[0]
+        reach = True if self.rank == 0 else can_reach(owner_bus)
+        if reach and self.rank != 0:
             shapes = [(lay.n_train, lay.n_train), (lay.n_test, lay.n_train)]
-            try:
-                mats = [SharedMatrix(r, c, handle=h) for (r, c), h in zip(shapes, box[0])]
-            except Exception:  # no peer access between these devices
-                mats, ok = [], 0.0
-        # every rank must agree on the placement: fall back to the gather if any import failed
-        flag = torch.tensor([ok], dtype=torch.float64,
-                            device="cpu" if dist.get_backend(self.group) == "gloo" else "cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
-        if flag.item() < 1.0:
+            mats = [SharedMatrix(r, c, handle=h) for (r, c), h in zip(shapes, handles)]
+        if not agree_placement(reach, self.group):
             for m in mats:
                 m.close()
             self.placement = "gather"
+            if self.rank == 0:
+                _log(f"placement: gather (a rank cannot store into {owner_bus})")
             return False
         self._shared = mats
         if self.rank == 0:
             self.K_train = mats[0].tensor()
             self.K_cross = mats[1].tensor() if lay.n_test else None
+            _log(f"placement: p2p, {self.world} ranks store into rank 0's matrices on "
+                 f"{owner_bus}")
         return True
 
     def _run_p2p(self, p_train, p_test, devc):
@@ -359,6 +434,11 @@ class KernelJob:
             return self._run_gather(p_train, p_test, devc)
         lay = self.layout
         lo, hi = lay.union_range(self.rank)  # one launch over this rank's joint tile range
+        # rank 0 may still be reading the matrices it returned from the previous run (they
+        # alias the shared memory): nobody stores until every rank has entered this run and
+        # drained its stream
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
         dev.job_into(p_train, p_test, self._shared[0].ptr,
                      self._shared[1].ptr if lay.n_test else 0, lo, hi)
         torch.cuda.current_stream().synchronize()  # this rank's stores have landed
@@ -412,10 +492,28 @@ class KernelJob:
         p_train = dev.gate_build(self.plan, train_angles)
         p_test = dev.gate_build(self.plan, test_angles) if self.layout.n_test else None
         if self.world == 1:
-            return self._run_local(p_train, p_test, train_angles.device)
-        if self.placement == "p2p":
-            return self._run_p2p(p_train, p_test, train_angles.device)
-        return self._run_gather(p_train, p_test, train_angles.device)
+            out = self._run_local(p_train, p_test, train_angles.device)
+        elif self.placement == "p2p":
+            out = self._run_p2p(p_train, p_test, train_angles.device)
+        else:
+            out = self._run_gather(p_train, p_test, train_angles.device)
+        if not torch.cuda.is_current_stream_capturing():
+            # every rank built every sample's planes, so every rank sees the same sentinel
+            self._check_finite(p_train, p_test)
+        return out
+
+    def _check_finite(self, p_train, p_test) -> None:
+        """The reference's RebindError for a non-finite angle (network.py:295-296), indexed
+        like the single-process API: the first Gram pair (row-major) holding a
+        bad train sample, else the first cross pair holding a bad test sample."""
+        bad = p_train.bad_sample()
+        if bad is not None:
+            raise RebindError(f"operand set {0 if bad == 0 else bad - 1}: feature angles must "
+                              "be finite")
+        bad = p_test.bad_sample() if p_test is not None else None
+        if bad is not None:
+            raise RebindError(f"operand set {bad * self.layout.n_train}: feature angles must "
+                              "be finite")
 
     def graph(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None):
         """CUDA-graph capture of :meth:`run` (world size 1): returns ``(replay, K_train,

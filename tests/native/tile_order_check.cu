@@ -2,7 +2,16 @@
 // every tile decoded exactly once, inside its matrix, super-rows contiguous in tile order.
 #include "qk_sweep.cu"
 #include <set>
-int main() {
+int main(int argc, char** argv) {
+  if (argc == 3) {  // "coords nb": the Gram tile list in kernel order, one "bi bj" per line
+    const int64_t nb = atoll(argv[2]);
+    for (int64_t g = 0; g < nb * (nb + 1) / 2; ++g) {
+      int64_t bi, bj;
+      qk::decode_upper(g, nb, bi, bj);
+      printf("%ld %ld\n", (long)bi, (long)bj);
+    }
+    return 0;
+  }
   for (int64_t nb : {1, 2, 7, 8, 9, 15, 16, 17, 157, 313}) {
     std::set<std::pair<int64_t,int64_t>> seen; int64_t nt = nb*(nb+1)/2; bool ok = true;
     for (int64_t g = 0; g < nt; ++g) { int64_t bi, bj; qk::decode_upper(g, nb, bi, bj);

@@ -85,6 +85,68 @@ def worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def placement_worker(rank, world, port, reach, q):
+    """KernelJob._setup_shared's placement protocol over gloo with the device calls faked:
+    rank 0 exports, the others check reachability of rank 0's device and import."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2405_02630_b200 import distributed as D
+
+    events = []
+
+    class FakeMatrix:
+        def __init__(self, rows, cols, handle=None):
+            events.append("import" if handle is not None else "alloc")
+            self.rows, self.cols, self.ptr = rows, cols, 1
+
+        def export(self):
+            return b"h" * 64
+
+        def tensor(self):
+            return torch.zeros((self.rows, self.cols), dtype=torch.float64)
+
+        def close(self):
+            events.append("close")
+
+    D.SharedMatrix = FakeMatrix
+    D.device_bus_id = lambda: "0000:1b:00.0"
+    D.can_reach = lambda bus: (bus == "0000:1b:00.0") and reach[rank]
+    job = D.KernelJob(SweepPlan(WIDTH, 2), N_TRAIN, N_TEST)
+    ok = job._setup_shared()
+    q.put((rank, ok, job.placement, events))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("reach", [(True, True, True), (True, True, False)])
+def test_p2p_placement_agreement_world3(reach):
+    """Every rank ends on the same placement: p2p only if every rank can reach rank 0's
+    device; otherwise all fall back to the gather and release what they mapped (a rank that
+    cannot reach rank 0 never attempts the import)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=placement_worker, args=(r, 3, port, reach, q))
+             for r in range(3)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    want = all(reach)
+    for rank, ok, placement, events in res:
+        assert ok == want and placement == ("p2p" if want else "gather")
+        if rank == 0:
+            assert events[:2] == ["alloc", "alloc"]
+        elif reach[rank]:
+            assert events[:2] == ["import", "import"]
+        else:
+            assert "import" not in events
+        if not want:
+            assert events.count("close") == events.count("alloc") + events.count("import")
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

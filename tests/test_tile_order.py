@@ -23,3 +23,13 @@ def test_tile_decode_is_a_bijection(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     lines = out.strip().splitlines()
     assert len(lines) == 10 and all(l.endswith(" ok") for l in lines), out
+    # the Python port of the Gram decode (per-rank entry counts) lists the same tiles in order
+    import numpy as np
+
+    from paper_2405_02630_b200.distributed import gram_tile_coords
+    for nb in (1, 7, 8, 9, 17, 157):
+        out = subprocess.run([str(exe), "coords", str(nb)], capture_output=True, text=True,
+                             check=True).stdout
+        want = np.array([[int(v) for v in l.split()] for l in out.strip().splitlines()])
+        bi, bj = gram_tile_coords(nb)
+        assert np.array_equal(np.stack([bi, bj], 1), want), nb
