@@ -65,6 +65,8 @@ _SIGNATURES = {
     "qk_job_tile_count": (_c_i64, [_c_vp, _c_i64, _c_i64]),
     "qk_job_tiles": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp,
                                     _c_vp, _c_vp]),
+    "qk_job_run": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp, _c_vp,
+                                  _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
     "qk_kernel_matrices_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp,
                                                _c_vp]),
     "qk_shared_alloc": (ctypes.c_int, [_c_sz, ctypes.POINTER(_c_vp)]),

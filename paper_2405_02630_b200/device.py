@@ -63,8 +63,12 @@ class Planes:
         return None if v == -1 else v
 
 
-def gate_build(plan: SweepPlan, angles: torch.Tensor, out: torch.Tensor | None = None) -> Planes:
-    """angles [N, width] fp64 (CUDA) -> planes (network.py:283-302 per sample)."""
+def gate_build(plan: SweepPlan, angles: torch.Tensor, out: torch.Tensor | None = None,
+               bad: torch.Tensor | None = None) -> Planes:
+    """angles [N, width] fp64 (CUDA) -> planes (network.py:283-302 per sample).
+
+    ``bad``: optional one-element int64 CUDA tensor already holding -1, the non-finite
+    sentinel to use (callers that build several plane sets reset theirs in one fill)."""
     _require(angles, "angles", torch.float64)
     if angles.dim() != 2 or angles.shape[1] != plan.width:
         raise RebindError(f"feature vectors of length {angles.shape[-1]} do not match width "
@@ -73,7 +77,8 @@ def gate_build(plan: SweepPlan, angles: torch.Tensor, out: torch.Tensor | None =
     nbytes = plan.planes_bytes(n)
     if out is None or out.numel() < nbytes:
         out = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=angles.device)
-    bad = torch.full((1,), -1, dtype=torch.int64, device=angles.device)
+    if bad is None:
+        bad = torch.full((1,), -1, dtype=torch.int64, device=angles.device)
     _native.check(_native.lib().qk_gate_build(plan.handle, angles.data_ptr(), n, plan.width,
                                               out.data_ptr(), bad.data_ptr(), _stream()))
     return Planes(plan, n, out, bad)

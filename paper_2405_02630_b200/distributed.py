@@ -358,9 +358,10 @@ class KernelJob:
     """Train Gram (+ optional test x train cross block) over a process group."""
 
     def __init__(self, plan: SweepPlan, n_train: int, n_test: int = 0, group=None,
-                 placement: str = "p2p"):
+                 placement: str = "p2p", graph_mode: bool | None = None):
         if placement not in ("p2p", "gather"):
             raise ValueError(f"unknown placement {placement!r}")
+        self.graph_mode = graph_mode  # None: auto (small single-GPU jobs replay a graph)
         self.plan = plan
         self.group = group
         self.placement = placement
@@ -374,6 +375,9 @@ class KernelJob:
         self.K_train = None
         self.K_cross = None
         self._shared = None
+        self._bad = None             # [2] int64 non-finite sentinels (train, test)
+        self._planes = [None, None]  # gate-plane buffers reused across runs
+        self._g = None               # captured single-GPU job (small jobs)
 
     # ---- world size 1 ----------------------------------------------------------------
     def _run_local(self, p_train, p_test, devc):
@@ -485,35 +489,119 @@ class KernelJob:
                                      seg.tile_end, self.K_cross)
         return self.K_train, self.K_cross
 
-    def run(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None):
-        """Returns (K_train, K_cross) on rank 0 (device tensors), (None, None) elsewhere."""
+    # Jobs below this many entry-qubits (~1 ms of sweep) replay a CUDA graph by default: the
+    # per-call host work of the eager path (~30-50 us) is comparable with the job itself.
+    GRAPH_ENTRY_QUBITS = 2e9
+
+    def run(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None,
+            check_finite: bool = True):
+        """Returns (K_train, K_cross) on rank 0 (device tensors), (None, None) elsewhere.
+
+        Single-GPU jobs of up to ~1 ms (``GRAPH_ENTRY_QUBITS``, unless ``graph_mode=False``)
+        run as a CUDA-graph replay of one qk_job_run (sentinel reset, both gate builds in
+        one launch, the sweep) after the inputs are copied into job-owned buffers.
+        ``check_finite`` (default) synchronises once to raise the reference's RebindError for
+        a non-finite angle; pass False to keep the call asynchronous."""
         from . import device as dev
 
-        p_train = dev.gate_build(self.plan, train_angles)
-        p_test = dev.gate_build(self.plan, test_angles) if self.layout.n_test else None
+        capturing = torch.cuda.is_current_stream_capturing()
+        if self.world == 1 and not capturing and self._graph_eligible():
+            self._run_graph(train_angles, test_angles)
+            if check_finite:
+                self._check_finite(self.layout.n_test > 0)
+            return self.K_train, self.K_cross
+        devc = train_angles.device
+        if self._bad is None or self._bad.device != devc:
+            self._bad = torch.empty(2, dtype=torch.int64, device=devc)
+            self._planes = [None, None]
+        self._bad.fill_(-1)  # both plane sets' non-finite sentinels, one fill
+        p_train = dev.gate_build(self.plan, train_angles, out=self._planes[0],
+                                 bad=self._bad[0:1])
+        self._planes[0] = p_train.buf
+        p_test = None
+        if self.layout.n_test:
+            p_test = dev.gate_build(self.plan, test_angles, out=self._planes[1],
+                                    bad=self._bad[1:2])
+            self._planes[1] = p_test.buf
         if self.world == 1:
-            out = self._run_local(p_train, p_test, train_angles.device)
+            out = self._run_local(p_train, p_test, devc)
         elif self.placement == "p2p":
-            out = self._run_p2p(p_train, p_test, train_angles.device)
+            out = self._run_p2p(p_train, p_test, devc)
         else:
-            out = self._run_gather(p_train, p_test, train_angles.device)
-        if not torch.cuda.is_current_stream_capturing():
+            out = self._run_gather(p_train, p_test, devc)
+        if check_finite and not capturing:
             # every rank built every sample's planes, so every rank sees the same sentinel
-            self._check_finite(p_train, p_test)
+            self._check_finite(p_test is not None)
         return out
 
-    def _check_finite(self, p_train, p_test) -> None:
+    def _graph_eligible(self) -> bool:
+        mode = getattr(self, "graph_mode", None)
+        if mode is not None:
+            return bool(mode)
+        return self.layout.entries() * self.plan.width <= self.GRAPH_ENTRY_QUBITS
+
+    def _run_graph(self, train_angles, test_angles) -> None:
+        from . import device as dev
+
+        lay, plan = self.layout, self.plan
+        dev._require(train_angles, "train angles", torch.float64)
+        if lay.n_test:
+            dev._require(test_angles, "test angles", torch.float64)
+        if train_angles.shape != (lay.n_train, plan.width) or (
+                lay.n_test and test_angles.shape != (lay.n_test, plan.width)):
+            raise RebindError(f"operand set 0: feature arrays of shapes "
+                              f"{tuple(train_angles.shape)} / "
+                              f"{tuple(test_angles.shape) if lay.n_test else ()} do not match "
+                              f"the job ({lay.n_train}, {lay.n_test}) x width {plan.width}")
+        devc = train_angles.device
+        if self._g is None or self._g_dev != devc:
+            f64 = dict(dtype=torch.float64, device=devc)
+            self._g_in = [torch.empty((lay.n_train, plan.width), **f64),
+                          torch.empty((max(lay.n_test, 1), plan.width), **f64)]
+            self._g_planes = [torch.empty(max(plan.planes_bytes(n), 16), dtype=torch.uint8,
+                                          device=devc) for n in (lay.n_train, lay.n_test)]
+            self._bad = torch.empty(2, dtype=torch.int64, device=devc)
+            self.K_train = torch.empty((lay.n_train, lay.n_train), **f64)
+            self.K_cross = torch.empty((lay.n_test, lay.n_train), **f64) if lay.n_test else None
+            lib = _native.lib()
+            nt = int(lib.qk_job_tile_count(plan.handle, lay.n_train, lay.n_test))
+
+            def body():
+                _native.check(lib.qk_job_run(
+                    plan.handle, self._g_in[0].data_ptr(), lay.n_train,
+                    self._g_in[1].data_ptr() if lay.n_test else None, lay.n_test,
+                    self._g_planes[0].data_ptr(),
+                    self._g_planes[1].data_ptr() if lay.n_test else None,
+                    self._bad.data_ptr(), 0, nt, self.K_train.data_ptr(),
+                    self.K_cross.data_ptr() if lay.n_test else None, dev._stream()))
+
+            side = torch.cuda.Stream(device=devc)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self._g_in[0].zero_()
+                self._g_in[1].zero_()
+                body()  # first use (launch caches), uncaptured
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                body()
+            self._g, self._g_dev = g, devc
+        self._g_in[0].copy_(train_angles)
+        if lay.n_test:
+            self._g_in[1].copy_(test_angles)
+        self._g.replay()
+
+    def _check_finite(self, has_test: bool) -> None:
         """The reference's RebindError for a non-finite angle (network.py:295-296), indexed
         like the single-process API: the first Gram pair (row-major) holding a
         bad train sample, else the first cross pair holding a bad test sample."""
-        bad = p_train.bad_sample()
-        if bad is not None:
-            raise RebindError(f"operand set {0 if bad == 0 else bad - 1}: feature angles must "
-                              "be finite")
-        bad = p_test.bad_sample() if p_test is not None else None
-        if bad is not None:
-            raise RebindError(f"operand set {bad * self.layout.n_train}: feature angles must "
-                              "be finite")
+        bad_train, bad_test = self._bad.tolist()  # one device sync for both sentinels
+        if bad_train != -1:
+            raise RebindError(f"operand set {0 if bad_train == 0 else bad_train - 1}: feature "
+                              "angles must be finite")
+        if has_test and bad_test != -1:
+            raise RebindError(f"operand set {bad_test * self.layout.n_train}: feature angles "
+                              "must be finite")
 
     def graph(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None):
         """CUDA-graph capture of :meth:`run` (world size 1): returns ``(replay, K_train,

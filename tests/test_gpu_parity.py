@@ -509,3 +509,35 @@ def test_kernel_job_graph_replay_matches_run(rng):
     torch.cuda.synchronize()
     K1, _ = KernelJob(SweepPlan(n, 2), N, M).run(tr, te)
     assert torch.equal(K, K1)
+
+
+@pytest.mark.parametrize("n", [50, 64])
+def test_kernel_job_auto_graph_matches_eager_and_api(rng, n):
+    """Small single-GPU jobs replay a captured qk_job_run by default: bit-identical to the
+    eager path and to the public API, fresh inputs every call (copied into the job's
+    buffers), and the reference's RebindError for a non-finite angle in either mode."""
+    N, M = 333, 71
+    cfg = FeatureMapConfig(n)
+    auto = KernelJob(SweepPlan(n, 2), N, M)
+    eager = KernelJob(SweepPlan(n, 2), N, M, graph_mode=False)
+    assert auto._graph_eligible() and not eager._graph_eligible()
+    for _ in range(3):
+        Xtr = rng.uniform(0, 0.3, (N, n))
+        Xte = rng.uniform(0, 0.3, (M, n))
+        tr, te = torch.as_tensor(Xtr, device="cuda"), torch.as_tensor(Xte, device="cuda")
+        K, Kx = auto.run(tr, te)
+        Ke, Kxe = eager.run(tr, te)
+        assert torch.equal(K, Ke) and torch.equal(Kx, Kxe)
+        assert np.array_equal(K.cpu().numpy(), compute_kernel_matrix(Xtr, cfg).entries)
+        assert np.array_equal(Kx.cpu().numpy(), compute_cross_kernel(Xte, Xtr, cfg).entries)
+    assert auto._g is not None
+    bad_tr = tr.clone()
+    bad_tr[7, 3] = float("nan")
+    for job in (auto, eager):
+        with pytest.raises(RebindError, match="operand set 6: feature angles must be finite"):
+            job.run(bad_tr, te)
+        bad_te = te.clone()
+        bad_te[2, 0] = float("inf")
+        with pytest.raises(RebindError, match=f"operand set {2 * N}: feature angles must be"):
+            job.run(tr, bad_te)
+        job.run(tr, te)  # the sentinels reset on the next call
