@@ -542,36 +542,56 @@ struct GateSet {
   int64_t blk0, nblk;
 };
 
-// One CTA = one plane block (64 samples) x 64 plane qubits.  Thread (t = tid % 64,
-// u = tid / 64) owns sample t and the qubit quads u, u + 4, u + 8, u + 12 of the slab: it
-// issues all of its angle loads first — VEC: each quad is one 32-byte sector of the sample's
-// row (two 16 B loads), so every fetched sector is used whole — then computes the 16
-// (cos, sin) pairs and stores them, a warp writing 32 consecutive samples of one qubit (512
-// contiguous bytes).  No shared memory, no barrier: the loads of the next quads overlap the
-// sincos of the previous ones.  Padding samples (front of block 0) and the identity qubits of
-// the width padding (front of the chain) get angle 0.  A second plane set (e.g. the test
-// samples of a joint job) rides in the same launch: blockIdx.x >= s0.nblk selects it.
-constexpr int kGateQuads = 4;                       // quads per thread
-constexpr int kGateQubits = 4 * 4 * kGateQuads;     // 64 plane qubits per CTA
+// Work item = one plane block (64 samples) x one 32-qubit slab.  Thread (t = tid % 64,
+// u = tid / 64) owns sample t and the qubit quads u and u + 4 of the slab.  VEC: each quad is
+// one 32-byte sector of the sample's row (two 16 B loads), so every fetched sector is used
+// whole.  Stores: a warp writes 32 consecutive samples of one qubit (512 contiguous bytes).
+// Persistent grid-stride CTAs with a register double buffer: the loads of the CTA's next item
+// are in flight while the sincos and stores of the current one run.  Padding samples (front
+// of block 0) and the identity qubits of the width padding (front of the chain) get angle 0.
+// A second plane set (e.g. the test samples of a joint job) rides in the same launch.
+constexpr int kGateQuads = 2;                    // quads per thread and item
+constexpr int kGateQubits = 4 * 4 * kGateQuads;  // 32 plane qubits per item
+
+struct GateItem {
+  const double* X;
+  int64_t ld;
+  double2* planes;
+  unsigned long long* bad;
+  int64_t blk, s;
+  int q_slab;
+  bool live;
+};
+
+// (field selects, not a pointer to the parameter, so the sets stay in the constant bank)
+__device__ __forceinline__ GateItem gate_item(const GateSet& s0, const GateSet& s1, int slabs,
+                                              int64_t item) {
+  GateItem g;
+  const int64_t b = item / slabs;
+  g.q_slab = int(item - b * slabs) * kGateQubits;
+  const bool second = b >= s0.nblk;
+  g.X = second ? s1.X : s0.X;
+  g.ld = second ? s1.ld : s0.ld;
+  g.planes = second ? s1.planes : s0.planes;
+  g.bad = second ? s1.bad : s0.bad;
+  const int64_t n = second ? s1.n : s0.n;
+  g.blk = second ? s1.blk0 + b - s0.nblk : s0.blk0 + b;
+  g.s = g.blk * kTile + (threadIdx.x & 63) - sample_pad(n);
+  g.live = g.s >= 0 && g.s < n;
+  return g;
+}
+
 template <bool VEC>
-__global__ void __launch_bounds__(256) gate_build_kernel(GateSet s0, GateSet s1, int width,
-                                                         int n_pad, int front, int half) {
-  const bool second = blockIdx.x >= s0.nblk;
-  const GateSet& gs = second ? s1 : s0;
-  const int64_t blk = gs.blk0 + (second ? blockIdx.x - s0.nblk : blockIdx.x);
-  const int t = threadIdx.x & 63, u = threadIdx.x >> 6;
-  const int64_t s = blk * kTile + t - sample_pad(gs.n);
-  const bool live = s >= 0 && s < gs.n;
-  const double* row = gs.X + (live ? s : 0) * gs.ld;
-  const int q_slab = blockIdx.y * kGateQubits;
-  double x[kGateQuads][4];
+__device__ __forceinline__ void gate_load(const GateItem& g, int width, int front,
+                                          double (&x)[kGateQuads][4]) {
+  const int u = threadIdx.x >> 6;
+  const double* row = g.X + (g.live ? g.s : 0) * g.ld;
 #pragma unroll
   for (int k = 0; k < kGateQuads; ++k) {
-    const int q0 = q_slab + 4 * (u + 4 * k);  // plane qubit of element 0 of the quad
-    const int qi = q0 - front;                // its input qubit
+    const int qi = g.q_slab + 4 * (u + 4 * k) - front;  // input qubit of element 0
     if (VEC) {
       // front % 4 == 0 and n_pad % 4 == 0: a quad is wholly input qubits or wholly padding
-      if (live && qi >= 0 && qi < width) {
+      if (g.live && qi >= 0 && qi < width) {
         const double2 lo = __ldg(reinterpret_cast<const double2*>(row + qi));
         const double2 hi = __ldg(reinterpret_cast<const double2*>(row + qi) + 1);
         x[k][0] = lo.x, x[k][1] = lo.y, x[k][2] = hi.x, x[k][3] = hi.y;
@@ -581,21 +601,26 @@ __global__ void __launch_bounds__(256) gate_build_kernel(GateSet s0, GateSet s1,
     } else {
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        x[k][e] = live && qi + e >= 0 && qi + e < width ? __ldg(row + qi + e) : 0.0;
+        x[k][e] = g.live && qi + e >= 0 && qi + e < width ? __ldg(row + qi + e) : 0.0;
     }
   }
-  if (gs.bad != nullptr) {
+}
+
+__device__ __forceinline__ void gate_store(const GateItem& g, int n_pad, int half,
+                                           const double (&x)[kGateQuads][4]) {
+  if (g.bad != nullptr) {
     bool finite = true;
 #pragma unroll
     for (int k = 0; k < kGateQuads; ++k)
 #pragma unroll
       for (int e = 0; e < 4; ++e) finite = finite && isfinite(x[k][e]);
-    if (!finite) atomicMin(gs.bad, (unsigned long long)s);  // padding values are 0: live
+    if (!finite) atomicMin(g.bad, (unsigned long long)g.s);  // padding values are 0
   }
-  double2* out = gs.planes + blk * int64_t(n_pad) * kTile + t;
+  const int u = threadIdx.x >> 6;
+  double2* out = g.planes + g.blk * int64_t(n_pad) * kTile + (threadIdx.x & 63);
 #pragma unroll
   for (int k = 0; k < kGateQuads; ++k) {
-    const int q0 = q_slab + 4 * (u + 4 * k);
+    const int q0 = g.q_slab + 4 * (u + 4 * k);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (q0 + e < n_pad) {
@@ -604,6 +629,35 @@ __global__ void __launch_bounds__(256) gate_build_kernel(GateSet s0, GateSet s1,
         out[int64_t(q0 + e) * kTile] = make_double2(cs, sn);
       }
     }
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256, 4) gate_build_kernel(GateSet s0, GateSet s1, int width,
+                                                         int n_pad, int front, int half) {
+  const int slabs = (n_pad + kGateQubits - 1) / kGateQubits;
+  const int64_t n_items = (s0.nblk + s1.nblk) * slabs;
+  int64_t it = blockIdx.x;
+  if (it >= n_items) return;
+  double xa[kGateQuads][4], xb[kGateQuads][4];
+  GateItem ga = gate_item(s0, s1, slabs, it);
+  gate_load<VEC>(ga, width, front, xa);
+  for (;;) {  // two items per trip so the double buffer needs no register moves
+    const int64_t nb = it + gridDim.x;
+    GateItem gb;
+    if (nb < n_items) {
+      gb = gate_item(s0, s1, slabs, nb);
+      gate_load<VEC>(gb, width, front, xb);
+    }
+    gate_store(ga, n_pad, half, xa);
+    if (nb >= n_items) break;
+    it = nb + gridDim.x;
+    if (it < n_items) {
+      ga = gate_item(s0, s1, slabs, it);
+      gate_load<VEC>(ga, width, front, xa);
+    }
+    gate_store(gb, n_pad, half, xb);
+    if (it >= n_items) break;
   }
 }
 
@@ -1335,14 +1389,15 @@ static qk_status launch_gate_sets(const Plan& p, GateSet s0, GateSet s1, cudaStr
   auto al32 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 31u) == 0; };
   const bool vec = p.front_pad % 4 == 0 && s0.ld % 4 == 0 && al32(s0.X) &&
                    (s1.nblk == 0 || (s1.ld % 4 == 0 && al32(s1.X)));
-  dim3 grid(unsigned(nb), unsigned((p.width_padded + kGateQubits - 1) / kGateQubits));
+  const int64_t items = nb * ((p.width_padded + kGateQubits - 1) / kGateQubits);
   const int half = p.layers == 2 ? 0 : 1;
-  if (vec)
-    gate_build_kernel<true><<<grid, 256, 0, st>>>(s0, s1, p.width, p.width_padded, p.front_pad,
-                                                  half);
-  else
-    gate_build_kernel<false><<<grid, 256, 0, st>>>(s0, s1, p.width, p.width_padded,
-                                                   p.front_pad, half);
+  auto kern = vec ? gate_build_kernel<true> : gate_build_kernel<false>;
+  int per_sm = 0;
+  if (qk_status s = resident_ctas(kern, 256, 0, &per_sm)) return s;
+  const int sms = sm_count();
+  if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
+  const int64_t grid = std::min<int64_t>(items, int64_t(sms) * per_sm);
+  kern<<<unsigned(grid), 256, 0, st>>>(s0, s1, p.width, p.width_padded, p.front_pad, half);
   return cuda_status(cudaGetLastError(), "gate_build launch");
 }
 

@@ -124,9 +124,13 @@ def config_data(config_id: int, n_train: int, n_test: int, kind: str = "mnist",
     """Angles for one config: seed = 240502630 + config_id."""
     seed = 240502630 + config_id
     if binary is not None:
-        X, y = synthetic_images(4 * (n_train + n_test), kind, seed, classes, mix)
+        # balanced labels: the binary classes are len(binary)/classes of the draw
+        draw = -(-(n_train + n_test) * classes // len(binary))
+        X, y = synthetic_images(draw, kind, seed, classes, mix)
         keep = np.isin(y, binary)
         X, y = X[keep][: n_train + n_test], y[keep][: n_train + n_test]
+        if len(y) < n_train + n_test:  # pragma: no cover - balanced draw always suffices
+            raise ValueError("not enough samples of the binary classes")
     else:
         X, y = synthetic_images(n_train + n_test, kind, seed, classes, mix)
     Xtr, ytr, Xte, yte = X[:n_train], y[:n_train], X[n_train:], y[n_train:]

@@ -1,6 +1,7 @@
 """Host-pipeline phase timing (QK_TRACE=1 prints h2d / gate / sweep / tail / host per call):
 config 4 (10,000 x 784 train, 2,000 test) through compute_kernel_matrices with pinned
-buffers.  usage: QK_TRACE=1 [QK_HEAD_SPLIT=0] python tools/e2e_trace.py [calls]"""
+buffers, or (--pageable) plain numpy arrays in and fresh ones out.
+usage: QK_TRACE=1 [QK_HEAD_SPLIT=0] python tools/e2e_trace.py [calls] [--pageable]"""
 import sys
 import time
 from pathlib import Path
@@ -18,13 +19,17 @@ def pin(a):
     return t
 
 
+pageable = "--pageable" in sys.argv
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
 rng = np.random.default_rng(0)
-X = pin(rng.uniform(0, np.pi, (10000, 784)))
-T = pin(rng.uniform(0, np.pi, (2000, 784)))
-K = pin(np.empty((10000, 10000)))
-Kx = pin(np.empty((2000, 10000)))
+X = rng.uniform(0, np.pi, (10000, 784))
+T = rng.uniform(0, np.pi, (2000, 784))
+kw = {}
+if not pageable:
+    X, T = pin(X), pin(T)
+    kw = {"out_train": pin(np.empty((10000, 10000))), "out_test": pin(np.empty((2000, 10000)))}
 cfg = FeatureMapConfig(784)
-for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 4):
+for _ in range(int(args[0]) if args else 4):
     t = time.perf_counter()
-    compute_kernel_matrices(X, T, cfg, out_train=K, out_test=Kx)
+    compute_kernel_matrices(X, T, cfg, **kw)
     print(f"wall {(time.perf_counter() - t) * 1e3:.3f} ms", flush=True)

@@ -8,7 +8,7 @@ The 784-qubit configs use bandwidth-scaled angles (median off-diagonal K in [1e-
 SURVEY.md §8(d)) on overlapping classes (data.synthetic_images(mix=0.6)), so one-vs-rest
 accuracy is well below 1 and "identical predictions" is a real gate.
 
-usage: python tools/parity_report.py [out.json] [--configs 1,2,3,4]
+usage: python tools/parity_report.py [out.json] [--configs 1,2,3,4] [--merge earlier.json]
 Writes the JSON report (partial results after every chunk, so a cut-off run still leaves
 evidence) and prints it at the end.  Reference: PAPER.md:322-326 (10-class accuracy table),
 SPEC.md:407-424, engine.py:132-166."""
@@ -80,6 +80,7 @@ def case(cid, n_tr, n_te, kind, *, features=None, binary=None, bw=1.0, mix=0.0, 
          progress=None):
     Atr, ytr, Ate, yte = config_data(cid, n_tr, n_te, kind, features=features, binary=binary,
                                      bw=bw, mix=mix)
+    assert (len(Atr), len(Ate)) == (n_tr, n_te), (len(Atr), len(Ate))
     cfg = FeatureMapConfig(Atr.shape[1])
     t = time.perf_counter()
     K, Kx = compute_kernel_matrices(Atr, Ate, cfg)
@@ -132,7 +133,8 @@ CASES = {
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    args = [a for k, a in enumerate(sys.argv[1:], 1)
+            if not a.startswith("--") and sys.argv[k - 1] not in ("--configs", "--merge")]
     out = Path(args[0]) if args else None
     cfgs = [1, 2, 3, 4]
     if "--configs" in sys.argv:
@@ -155,8 +157,12 @@ def main():
         rep["progress"] = p
         dump()
 
+    if "--merge" in sys.argv:  # keep the other configs' cases of an earlier report
+        old = json.loads(Path(sys.argv[sys.argv.index("--merge") + 1]).read_text())
+        rep["cases"] = [c for c in old["cases"] if c["config"] not in cfgs]
     for c in cfgs:
         rep["cases"].append(case(**CASES[c], progress=progress))
+        rep["cases"].sort(key=lambda c: c["config"])
         rep["progress"] = None
         dump()
     rep["all_within_1e-12"] = all(c["within_1e-12"] for c in rep["cases"])

@@ -1,6 +1,7 @@
 """Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck /
-synccheck): gate build, joint sweep (L = 1..8), dense + packed + unpack, pair kernel,
-host pipelines (pinned and pageable)."""
+synccheck): gate build (vector and scalar loads, one and two plane sets), joint sweep
+(L = 1..8), dense + packed + unpack, pair kernel, host pipelines (pinned and pageable, the
+head-first two-stream upload), and the CUDA-graph replay of qk_job_run (KernelJob)."""
 import sys
 from pathlib import Path
 
@@ -36,4 +37,20 @@ for L, n in ((2, 40), (1, 20), (3, 6), (4, 5), (5, 4), (6, 3), (7, 3), (8, 2)):
 pinned = torch.empty((150, 150), dtype=torch.float64, pin_memory=True).numpy()
 compute_kernel_matrices(rng.uniform(0, 1, (150, 40)), rng.uniform(0, 1, (3, 40)),
                         FeatureMapConfig(40), out_train=pinned)
+# head-first pipeline (pinned inputs large enough for a head: 1100 samples at 784 qubits)
+Xh = torch.empty((1100, 784), dtype=torch.float64, pin_memory=True).numpy()
+Xh[:] = rng.uniform(0, 0.05, Xh.shape)
+Th = torch.empty((70, 784), dtype=torch.float64, pin_memory=True).numpy()
+Th[:] = rng.uniform(0, 0.05, Th.shape)
+Kh, Kxh = compute_kernel_matrices(Xh, Th, FeatureMapConfig(784))
+Kh2, Kxh2 = compute_kernel_matrices(np.array(Xh), np.array(Th), FeatureMapConfig(784))
+assert np.array_equal(Kh.entries, Kh2.entries) and np.array_equal(Kxh.entries, Kxh2.entries)
+# the small-job graph path (vector gate build at 64 qubits, scalar at 50)
+from paper_2405_02630_b200.distributed import KernelJob  # noqa: E402
+for n in (64, 50):
+    tr = torch.as_tensor(rng.uniform(0, 1, (200, n)), device="cuda")
+    te = torch.as_tensor(rng.uniform(0, 1, (30, n)), device="cuda")
+    Kg, Kxg = KernelJob(SweepPlan(n, 2), 200, 30).run(tr, te)
+    Ke, Kxe = KernelJob(SweepPlan(n, 2), 200, 30, graph_mode=False).run(tr, te)
+    assert torch.equal(Kg, Ke) and torch.equal(Kxg, Kxe)
 print("sanitize smoke ok")
