@@ -44,6 +44,20 @@ struct Workspace {
   void* stage[2] = {nullptr, nullptr};  // pinned staging for pageable host buffers
   size_t stage_cap = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  void* in_stage = nullptr;  // pinned copy of pageable angle arrays (head-first upload)
+  size_t in_stage_cap = 0;
+
+  qk_status ensure_in_stage(size_t bytes) {
+    if (in_stage_cap >= bytes) return QK_OK;
+    if (in_stage) cudaFreeHost(in_stage);
+    in_stage = nullptr;
+    in_stage_cap = 0;
+    if (cudaError_t e = cudaHostAlloc(&in_stage, bytes, cudaHostAllocDefault))
+      return set_error(QK_ERR_CAPACITY, std::string("pinned input staging allocation failed: ") +
+                                            cudaGetErrorString(e));
+    in_stage_cap = bytes;
+    return QK_OK;
+  }
 
   qk_status ensure_stage(size_t bytes) {
     if (stage_cap >= bytes) return QK_OK;
@@ -136,7 +150,7 @@ class CopyPool {
   }
   // copies n bytes src -> dst in parallel; blocks until done
   void copy(void* dst, const void* src, size_t n) {
-    const size_t parts = std::min<size_t>(workers_.size(), std::max<size_t>(1, n >> 22));
+    const size_t parts = std::min<size_t>(workers_.size(), std::max<size_t>(1, n >> 20));
     if (parts <= 1) {
       std::memcpy(dst, src, n);
       return;
@@ -388,12 +402,17 @@ StreamWaitValue32Fn stream_wait_value32() {
 // gate-built, the sweep runs the B x B Gram head (decode_gram orders it first) while the rest
 // of the angles upload on the h2d stream, then the rest is gate-built and swept.  B is the
 // smallest multiple of kGroup whose head keeps the GPU busy for as long as the remaining
-// upload takes (estimates: ~0.6 us per tile per qubit on 148 SMs, ~50 GB/s of H2D).
-int64_t choose_head(const Plan& p, int64_t n_train, int64_t n_test) {
+// upload takes (estimates: ~0.6 us per tile per qubit on 148 SMs, ~50 GB/s of H2D from pinned
+// buffers; ~12 GB/s for pageable ones, which the host first copies into pinned staging).
+bool head_split_enabled(const Plan& p) {
   const char* v = getenv("QK_HEAD_SPLIT");
-  if ((v != nullptr && v[0] == '0') || p.layers != 2) return 0;
+  return !(v != nullptr && v[0] == '0') && p.layers == 2;
+}
+
+int64_t choose_head(const Plan& p, int64_t n_train, int64_t n_test, double bw_bytes_per_ms) {
+  if (!head_split_enabled(p)) return 0;
   const int64_t nb = blocks_for(n_train), pad = sample_pad(n_train);
-  const double tile_ms = 6e-4 * p.width, bw_bytes_per_ms = 50e6;
+  const double tile_ms = 6e-4 * p.width;
   for (int64_t B = kGroup; B + kGroup <= nb; B += kGroup) {
     const int64_t s1 = std::min<int64_t>(n_train, B * kTile - pad);
     const double rest_ms = double((n_train - s1) + n_test) * p.width * 8 / bw_bytes_per_ms;
@@ -498,33 +517,44 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
     cudaEventDestroy(fin);
   }
   cudaStreamQuery(w->stream);  // flush the launch to the device before host-blocking work
-  // flat list of panels (target, panel index); panel sr = tile rows [sr*panel_rows, +panel_rows)
-  std::vector<std::pair<int, int64_t>> panels;
-  for (int k = 0; k < n_targets; ++k)
-    for (int64_t sr = 0; sr < (blocks_for(tg[k].n_rows) + panel_rows - 1) / panel_rows; ++sr)
-      panels.emplace_back(k, sr);
+  // flat list of panels (target, tile rows [r0, r1)), in the order the sweep finishes them:
+  // panel_rows tile rows each, except that the LAST target's final kGroup tile rows go out one
+  // tile row at a time, so the copy that trails the sweep is one 64-row panel
+  struct Panel {
+    int k;
+    int64_t r0, r1;
+  };
+  std::vector<Panel> panels;
+  for (int k = 0; k < n_targets; ++k) {
+    const int64_t nbr = blocks_for(tg[k].n_rows);
+    const int64_t fine_from = k == n_targets - 1 ? std::max<int64_t>(0, nbr - kGroup) : nbr;
+    for (int64_t r0 = 0; r0 < nbr;) {
+      const int64_t step = r0 >= fine_from ? 1 : panel_rows;
+      const int64_t r1 = std::min(std::min(r0 + step, nbr), r0 < fine_from ? fine_from : nbr);
+      panels.push_back({k, r0, r1});
+      r0 = r1;
+    }
+  }
   const uint32_t unit = progress_unit(p.layers);
-  auto rows_of = [&](int k, int64_t sr, int64_t& i0, int64_t& i1) {
+  auto rows_of = [&](const Panel& pn, int64_t& i0, int64_t& i1) {
     // sample rows of the panel (the front padding of block 0 is not a sample)
-    const int64_t pad = sample_pad(tg[k].n_rows);
-    i0 = std::max<int64_t>(0, sr * panel_rows * kTile - pad);
-    i1 = std::min<int64_t>((sr + 1) * panel_rows * kTile - pad, tg[k].n_rows);
+    const int64_t pad = sample_pad(tg[pn.k].n_rows);
+    i0 = std::max<int64_t>(0, pn.r0 * kTile - pad);
+    i1 = std::min<int64_t>(pn.r1 * kTile - pad, tg[pn.k].n_rows);
   };
   auto enqueue = [&](size_t idx, void* dst) -> cudaError_t {
-    const int k = panels[idx].first;
-    const int64_t sr = panels[idx].second;
-    const DrainTarget& t = tg[k];
+    const Panel& pn = panels[idx];
+    const DrainTarget& t = tg[pn.k];
     if (t.d_prog != nullptr) {
       const int64_t nbr = blocks_for(t.n_rows), nbc = blocks_for(t.n_cols);
-      const int64_t r0 = sr * panel_rows, r1 = std::min<int64_t>(r0 + panel_rows, nbr);
-      for (int64_t r = r0; r < r1; ++r) {  // every tile row of the panel is complete
+      for (int64_t r = pn.r0; r < pn.r1; ++r) {  // every tile row of the panel is complete
         const uint32_t expect = unit * uint32_t(t.mode == kModeGram ? nbr - r : nbc);
         if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + r), expect, 0x0) != 0)
           return cudaErrorNotSupported;
       }
     }
     int64_t i0, i1;
-    rows_of(k, sr, i0, i1);
+    rows_of(pn, i0, i1);
     return cudaMemcpyAsync(dst, t.d_K + i0 * t.n_cols,
                            size_t(i1 - i0) * t.n_cols * sizeof(double), cudaMemcpyDeviceToHost,
                            cs);
@@ -588,9 +618,9 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
       const int slot = int(idx & 1);
       e = cudaEventSynchronize(w->stage_ev[slot]);
       if (e != cudaSuccess) break;
-      const DrainTarget& t = tg[panels[idx].first];
+      const DrainTarget& t = tg[panels[idx].k];
       int64_t i0, i1;
-      rows_of(panels[idx].first, panels[idx].second, i0, i1);
+      rows_of(panels[idx], i0, i1);
       copy_pool().copy(t.h_K + i0 * t.n_cols, w->stage[slot],
                        size_t(i1 - i0) * t.n_cols * sizeof(double));
       if (idx + 2 < np) {
@@ -697,16 +727,27 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
                        {dKs, h_K_cross, n_test, n_train, kModeCross, nullptr}};
   const int64_t nt = qk_job_tile_count(plan, n_train, n_test);
   const int n_targets = n_test > 0 ? 2 : 1;
-  const int64_t B = is_pinned(h_train) && (n_test == 0 || is_pinned(h_test))
-                        ? choose_head(*p, n_train, n_test)
-                        : 0;
+  // Head-first upload (module comment above choose_head).  Pageable angle arrays are copied
+  // into a pinned staging buffer by the host copy pool: the head rows before the head's
+  // upload, the rest while the head sweeps.
+  const bool pin_in = is_pinned(h_train) && (n_test == 0 || is_pinned(h_test));
+  const int64_t B = choose_head(*p, n_train, n_test, pin_in ? 50e6 : 12e6);
+  const bool staged = B > 0 && !pin_in;
+  const double* src_tr = h_train;
+  const double* src_te = h_test;
+  if (staged) {
+    if (qk_status s = w->ensure_in_stage(xtb + xsb)) return s;
+    src_tr = static_cast<const double*>(w->in_stage);
+    src_te = src_tr + size_t(n_train) * p->width;
+  }
   if (B > 0) {
     // head: its angles, its planes, then the head sweep with the rest uploading beside it
     const int64_t s1 = std::min<int64_t>(n_train, B * kTile - sample_pad(n_train));
     const size_t row = size_t(p->width) * sizeof(double);
+    if (staged) copy_pool().copy(w->in_stage, h_train, size_t(s1) * row);
     if (cudaError_t e = cudaMemsetAsync(w->bad, 0xFF, 2 * sizeof(uint64_t), st))
       return cuda_err(e, "sentinel reset");
-    if (cudaError_t e = cudaMemcpyAsync(dXt, h_train, size_t(s1) * row, cudaMemcpyHostToDevice,
+    if (cudaError_t e = cudaMemcpyAsync(dXt, src_tr, size_t(s1) * row, cudaMemcpyHostToDevice,
                                         st))
       return cuda_err(e, "H2D head");
     trace.mark(1, st);
@@ -736,11 +777,18 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, 0, n_head, dKt, dKs, st,
                                         tg[0].d_prog, tg[1].d_prog, B))
             return s2;
-          cudaError_t e = cudaMemcpyAsync(dXt + s1 * p->width, h_train + s1 * p->width,
+          if (staged) {  // host copies of the rest while the head sweeps
+            cudaStreamQuery(st);  // flush the head launch to the device first
+            copy_pool().copy(static_cast<char*>(w->in_stage) + size_t(s1) * row,
+                             h_train + s1 * p->width, size_t(n_train - s1) * row);
+            if (n_test > 0)
+              copy_pool().copy(const_cast<double*>(src_te), h_test, xsb);
+          }
+          cudaError_t e = cudaMemcpyAsync(dXt + s1 * p->width, src_tr + s1 * p->width,
                                           size_t(n_train - s1) * row, cudaMemcpyHostToDevice,
                                           hs);
           if (e == cudaSuccess && n_test > 0)
-            e = cudaMemcpyAsync(dXs, h_test, xsb, cudaMemcpyHostToDevice, hs);
+            e = cudaMemcpyAsync(dXs, src_te, xsb, cudaMemcpyHostToDevice, hs);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev[0], 0);  // head planes, resets
           // on a failure past this point, let the rest's queued work finish before returning
           // (it reads and writes the workspace the next call reuses)

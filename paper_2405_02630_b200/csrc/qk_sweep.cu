@@ -542,17 +542,15 @@ struct GateSet {
   int64_t blk0, nblk;
 };
 
-// Work item = one plane block (64 samples) x one 32-qubit slab.  Thread (t = tid % 64,
-// u = tid / 64) owns sample t and the qubit quads u and u + 4 of the slab.  VEC: each quad is
-// one 32-byte sector of the sample's row (two 16 B loads), so every fetched sector is used
-// whole.  Stores: a warp writes 32 consecutive samples of one qubit (512 contiguous bytes).
-// Persistent grid-stride CTAs with a register double buffer: the loads of the CTA's next item
-// are in flight while the sincos and stores of the current one run.  Padding samples (front
-// of block 0) and the identity qubits of the width padding (front of the chain) get angle 0.
+// Work item = one plane block (64 samples) x one slab of 16 * QD plane qubits.  Thread
+// (t = tid % 64, u = tid / 64) owns sample t and the qubit quads u, u + 4, ... of the slab.
+// VEC: each quad is one 32-byte sector of the sample's row (two 16 B loads), so every fetched
+// sector is used whole; all of a thread's loads are issued before its first sincos.  Stores:
+// a warp writes 32 consecutive samples of one qubit (512 contiguous bytes).  PERSIST: grid-
+// stride CTAs with a register double buffer (the next item's loads in flight during the
+// current item's sincos and stores); otherwise one CTA per item.  Padding samples (front of
+// block 0) and the identity qubits of the width padding (front of the chain) get angle 0.
 // A second plane set (e.g. the test samples of a joint job) rides in the same launch.
-constexpr int kGateQuads = 2;                    // quads per thread and item
-constexpr int kGateQubits = 4 * 4 * kGateQuads;  // 32 plane qubits per item
-
 struct GateItem {
   const double* X;
   int64_t ld;
@@ -564,11 +562,12 @@ struct GateItem {
 };
 
 // (field selects, not a pointer to the parameter, so the sets stay in the constant bank)
+template <int QD>
 __device__ __forceinline__ GateItem gate_item(const GateSet& s0, const GateSet& s1, int slabs,
                                               int64_t item) {
   GateItem g;
   const int64_t b = item / slabs;
-  g.q_slab = int(item - b * slabs) * kGateQubits;
+  g.q_slab = int(item - b * slabs) * 16 * QD;
   const bool second = b >= s0.nblk;
   g.X = second ? s1.X : s0.X;
   g.ld = second ? s1.ld : s0.ld;
@@ -581,13 +580,13 @@ __device__ __forceinline__ GateItem gate_item(const GateSet& s0, const GateSet& 
   return g;
 }
 
-template <bool VEC>
+template <bool VEC, int QD>
 __device__ __forceinline__ void gate_load(const GateItem& g, int width, int front,
-                                          double (&x)[kGateQuads][4]) {
+                                          double (&x)[QD][4]) {
   const int u = threadIdx.x >> 6;
   const double* row = g.X + (g.live ? g.s : 0) * g.ld;
 #pragma unroll
-  for (int k = 0; k < kGateQuads; ++k) {
+  for (int k = 0; k < QD; ++k) {
     const int qi = g.q_slab + 4 * (u + 4 * k) - front;  // input qubit of element 0
     if (VEC) {
       // front % 4 == 0 and n_pad % 4 == 0: a quad is wholly input qubits or wholly padding
@@ -606,12 +605,13 @@ __device__ __forceinline__ void gate_load(const GateItem& g, int width, int fron
   }
 }
 
+template <int QD>
 __device__ __forceinline__ void gate_store(const GateItem& g, int n_pad, int half,
-                                           const double (&x)[kGateQuads][4]) {
+                                           const double (&x)[QD][4]) {
   if (g.bad != nullptr) {
     bool finite = true;
 #pragma unroll
-    for (int k = 0; k < kGateQuads; ++k)
+    for (int k = 0; k < QD; ++k)
 #pragma unroll
       for (int e = 0; e < 4; ++e) finite = finite && isfinite(x[k][e]);
     if (!finite) atomicMin(g.bad, (unsigned long long)g.s);  // padding values are 0
@@ -619,7 +619,7 @@ __device__ __forceinline__ void gate_store(const GateItem& g, int n_pad, int hal
   const int u = threadIdx.x >> 6;
   double2* out = g.planes + g.blk * int64_t(n_pad) * kTile + (threadIdx.x & 63);
 #pragma unroll
-  for (int k = 0; k < kGateQuads; ++k) {
+  for (int k = 0; k < QD; ++k) {
     const int q0 = g.q_slab + 4 * (u + 4 * k);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -632,31 +632,36 @@ __device__ __forceinline__ void gate_store(const GateItem& g, int n_pad, int hal
   }
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(256, 4) gate_build_kernel(GateSet s0, GateSet s1, int width,
-                                                         int n_pad, int front, int half) {
-  const int slabs = (n_pad + kGateQubits - 1) / kGateQubits;
+template <bool VEC, int QD, bool PERSIST, int MINB>
+__global__ void __launch_bounds__(256, MINB) gate_build_kernel(GateSet s0, GateSet s1, int width,
+                                                               int n_pad, int front, int half) {
+  const int slabs = (n_pad + 16 * QD - 1) / (16 * QD);
   const int64_t n_items = (s0.nblk + s1.nblk) * slabs;
   int64_t it = blockIdx.x;
   if (it >= n_items) return;
-  double xa[kGateQuads][4], xb[kGateQuads][4];
-  GateItem ga = gate_item(s0, s1, slabs, it);
-  gate_load<VEC>(ga, width, front, xa);
+  double xa[QD][4];
+  GateItem ga = gate_item<QD>(s0, s1, slabs, it);
+  gate_load<VEC, QD>(ga, width, front, xa);
+  if (!PERSIST) {
+    gate_store<QD>(ga, n_pad, half, xa);
+    return;
+  }
+  double xb[QD][4];
   for (;;) {  // two items per trip so the double buffer needs no register moves
     const int64_t nb = it + gridDim.x;
     GateItem gb;
     if (nb < n_items) {
-      gb = gate_item(s0, s1, slabs, nb);
-      gate_load<VEC>(gb, width, front, xb);
+      gb = gate_item<QD>(s0, s1, slabs, nb);
+      gate_load<VEC, QD>(gb, width, front, xb);
     }
-    gate_store(ga, n_pad, half, xa);
+    gate_store<QD>(ga, n_pad, half, xa);
     if (nb >= n_items) break;
     it = nb + gridDim.x;
     if (it < n_items) {
-      ga = gate_item(s0, s1, slabs, it);
-      gate_load<VEC>(ga, width, front, xa);
+      ga = gate_item<QD>(s0, s1, slabs, it);
+      gate_load<VEC, QD>(ga, width, front, xa);
     }
-    gate_store(gb, n_pad, half, xb);
+    gate_store<QD>(gb, n_pad, half, xb);
     if (it >= n_items) break;
   }
 }
@@ -1389,15 +1394,46 @@ static qk_status launch_gate_sets(const Plan& p, GateSet s0, GateSet s1, cudaStr
   auto al32 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 31u) == 0; };
   const bool vec = p.front_pad % 4 == 0 && s0.ld % 4 == 0 && al32(s0.X) &&
                    (s1.nblk == 0 || (s1.ld % 4 == 0 && al32(s1.X)));
-  const int64_t items = nb * ((p.width_padded + kGateQubits - 1) / kGateQubits);
   const int half = p.layers == 2 ? 0 : 1;
-  auto kern = vec ? gate_build_kernel<true> : gate_build_kernel<false>;
-  int per_sm = 0;
-  if (qk_status s = resident_ctas(kern, 256, 0, &per_sm)) return s;
-  const int sms = sm_count();
-  if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
-  const int64_t grid = std::min<int64_t>(items, int64_t(sms) * per_sm);
-  kern<<<unsigned(grid), 256, 0, st>>>(s0, s1, p.width, p.width_padded, p.front_pad, half);
+  // QK_GATE_VARIANT (tuning): 0 = 4 quads/thread, one CTA per 64-qubit item (default);
+  // 1 = 2 quads, 32-qubit items; 2 = 2 quads, persistent double-buffered; 3 = as 0 with 5
+  // resident CTAs per SM
+  static const int variant = [] {
+    const char* v = getenv("QK_GATE_VARIANT");
+    return v == nullptr ? 0 : v[0] - '0';
+  }();
+  auto launch = [&](auto kern, int qd, bool persist) -> qk_status {
+    const int64_t items = nb * ((p.width_padded + 16 * qd - 1) / (16 * qd));
+    int64_t grid = items;
+    if (persist) {
+      int per_sm = 0;
+      if (qk_status s = resident_ctas(kern, 256, 0, &per_sm)) return s;
+      const int sms = sm_count();
+      if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
+      grid = std::min<int64_t>(items, int64_t(sms) * per_sm);
+    }
+    kern<<<unsigned(grid), 256, 0, st>>>(s0, s1, p.width, p.width_padded, p.front_pad, half);
+    return QK_OK;
+  };
+  qk_status ls;
+  switch (variant) {
+    case 1:
+      ls = vec ? launch(gate_build_kernel<true, 2, false, 1>, 2, false)
+               : launch(gate_build_kernel<false, 2, false, 1>, 2, false);
+      break;
+    case 2:
+      ls = vec ? launch(gate_build_kernel<true, 2, true, 4>, 2, true)
+               : launch(gate_build_kernel<false, 2, true, 4>, 2, true);
+      break;
+    case 3:
+      ls = vec ? launch(gate_build_kernel<true, 4, false, 5>, 4, false)
+               : launch(gate_build_kernel<false, 4, false, 5>, 4, false);
+      break;
+    default:
+      ls = vec ? launch(gate_build_kernel<true, 4, false, 1>, 4, false)
+               : launch(gate_build_kernel<false, 4, false, 1>, 4, false);
+  }
+  if (ls != QK_OK) return ls;
   return cuda_status(cudaGetLastError(), "gate_build launch");
 }
 

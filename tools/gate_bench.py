@@ -34,7 +34,7 @@ def case(n, n_a, n_b, reps=20):
         _native.check(lib.qk_job_run(plan.handle, A.data_ptr(), n_a,
                                      B.data_ptr() if n_b else None, n_b, pa.data_ptr(),
                                      pb.data_ptr() if n_b else None, bad.data_ptr(), 0, 0,
-                                     Ktr.data_ptr(), None, st))
+                                     Ktr.data_ptr(), Ktr.data_ptr() if n_b else None, st))
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
