@@ -149,10 +149,25 @@ class CopyPool {
     for (auto& t : workers_) t.join();
   }
   // copies n bytes src -> dst in parallel; blocks until done
-  void copy(void* dst, const void* src, size_t n) {
+  void copy(void* dst, const void* src, size_t n) { run(dst, src, n); }
+  // writes one byte of every 4 KB page of [dst, dst + n) in parallel: a fresh (never touched)
+  // pageable output buffer takes its page faults here, while the GPU is busy, instead of
+  // inside the drain copies that trail the sweep
+  void touch(void* dst, size_t n) { run(dst, nullptr, n); }
+
+ private:
+  static void work(char* d, const char* sp, size_t lo, size_t hi) {
+    if (sp != nullptr) {
+      std::memcpy(d + lo, sp + lo, hi - lo);
+      return;
+    }
+    for (size_t o = (lo + 4095) & ~size_t(4095); o < hi; o += 4096)
+      *reinterpret_cast<volatile char*>(d + o) = 0;
+  }
+  void run(void* dst, const void* src, size_t n) {
     const size_t parts = std::min<size_t>(workers_.size(), std::max<size_t>(1, n >> 20));
     if (parts <= 1) {
-      std::memcpy(dst, src, n);
+      work(static_cast<char*>(dst), static_cast<const char*>(src), 0, n);
       return;
     }
     std::lock_guard<std::mutex> one_caller(call_mu_);
@@ -167,8 +182,6 @@ class CopyPool {
     cv_.notify_all();
     done_cv_.wait(g, [this] { return done_ == parts_; });
   }
-
- private:
   void loop() {
     uint64_t seen = 0;
     std::unique_lock<std::mutex> g(mu_);
@@ -182,7 +195,7 @@ class CopyPool {
         char* d = dst_;
         const char* sp = src_;
         g.unlock();
-        std::memcpy(d + lo, sp + lo, hi - lo);
+        work(d, sp, lo, hi);
         g.lock();
         if (++done_ == parts_) done_cv_.notify_all();
       }
@@ -501,6 +514,12 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
     cudaEventDestroy(reset);
     return s;
   }
+  if (!all_pinned) {  // pageable outputs: take their page faults while the sweep runs
+    cudaStreamQuery(w->stream);
+    for (int k = 0; k < n_targets; ++k)
+      if (!is_pinned(tg[k].h_K))
+        copy_pool().touch(tg[k].h_K, size_t(tg[k].n_rows) * tg[k].n_cols * sizeof(double));
+  }
   if (trace) trace->mark(3, w->stream);
   cudaStream_t cs = w->copy_stream;
   if (!all_pinned) {  // the staging slots may still feed the H2D of the inputs
@@ -731,7 +750,11 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
   // into a pinned staging buffer by the host copy pool: the head rows before the head's
   // upload, the rest while the head sweeps.
   const bool pin_in = is_pinned(h_train) && (n_test == 0 || is_pinned(h_test));
-  const int64_t B = choose_head(*p, n_train, n_test, pin_in ? 50e6 : 12e6);
+  const bool pin_out = is_pinned(h_K_train) && (n_test == 0 || is_pinned(h_K_cross));
+  // a pageable output is drained by host copies that can only start on finished row panels,
+  // which a big head delays (the head's rows finish with their strip): keep the head at the
+  // pinned-upload size there and let the rest's staging stall the GPU briefly instead
+  const int64_t B = choose_head(*p, n_train, n_test, pin_in || !pin_out ? 50e6 : 12e6);
   const bool staged = B > 0 && !pin_in;
   const double* src_tr = h_train;
   const double* src_te = h_test;

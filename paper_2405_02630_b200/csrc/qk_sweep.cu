@@ -447,10 +447,6 @@ __device__ __forceinline__ double kernel_value(double amp, int convention) {
 // Fence between a tile's stores and its progress-counter bump (host pipelines only).  The
 // tile, the counter and the copy engine's reads all live in / go through this device's memory
 // and L2, so gpu scope suffices; a system-scope fence cost ~3 % of the sweep (measured).
-// Sweep epilogue: 0 = CTA-staged whole-row stores (two CTA barriers per tile), 1 = per-warp.
-#ifndef QK_EPI
-#define QK_EPI 0
-#endif
 
 #ifndef QK_PROGRESS_FENCE
 #define QK_PROGRESS_FENCE __threadfence
@@ -715,7 +711,11 @@ struct Claim {
   int half;   // -1: whole tile; 0 / 1: tile rows 0-31 / 32-63 only
 };
 
-template <int LAYERS, int MODE, int OUT, int RI>
+// EPI (sweep epilogue): 0 = CTA-staged whole-row stores (two CTA barriers per tile; the
+// default), 1 = per-warp stores straight from the registers and a warp-private transposing
+// stage for the Gram mirror (no CTA barrier: short chains, where a tile's sweep is only a few
+// microseconds and the CTA-wide epilogue would idle the FP64 pipe for a large share of it).
+template <int LAYERS, int MODE, int OUT, int RI, int EPI>
 __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   using St = typename BondT<LAYERS>::type;
   constexpr int kRI = Geo<RI>::kRI, kWarps = Geo<RI>::kWarps;
@@ -884,12 +884,14 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
           if (ty * kRI + r >= r_lo && ty * kRI + r < r_hi)
             o[(ty * kRI + r) * kTile + tx + kTX * c] =
                 kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
-    } else if (QK_EPI == 1) {
+    } else if (EPI == 1) {
       // Per-warp epilogue, no CTA barrier: the warp's 2*kRI rows go out straight from the
       // registers (each store instruction writes two 128 B row segments), and the Gram mirror
       // through a warp-private transposing stage in shared memory (each lane writes the
-      // warp's 2*kRI values of one or two rows of K).
+      // warp's 2*kRI values of one or two rows of K).  Warps outside the item's rows (a half
+      // tile) store nothing.
       constexpr int kWR = 2 * kRI;  // rows per warp
+      const bool mine = warp_row_end > r_lo && warp_row_end - kWR < r_hi;
       double* out = t.prob ? a.out2 : a.out;
       const int64_t ld = t.prob ? a.n_cols : a.ld_out;
       const int64_t n_rows = t.prob ? a.n_rows2 : a.n_rows;
@@ -902,14 +904,15 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
         for (int c = 0; c < kRJ; ++c) {
           v[r][c] = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
           const int64_t i = i0 + ty * kRI + r, j = j0 + tx + kTX * c;
-          if (gram) {
+          if (!mine) {
+          } else if (gram) {
             if (i >= 0 && i < n_rows && j < n_rows && i <= j)
               out[i * ld + j] = i == j ? 1.0 : v[r][c];
           } else if (i >= 0 && j >= 0 && i < n_rows && j < a.n_cols) {
             out[i * ld + j] = v[r][c];
           }
         }
-      if (gram) {
+      if (gram && mine) {
         const int w = tid / 32;
         double* wb = stage_T + w * (kWR * (kTile + 1));
         __syncwarp();  // this warp's mirror pass of the previous tile has read wb
@@ -979,9 +982,9 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   }
 }
 
-template <int LAYERS, int MODE, int OUT, int RI>
+template <int LAYERS, int MODE, int OUT, int RI, int EPI>
 __global__ void __launch_bounds__(Geo<RI>::kThreads, 1) sweep_kernel(const SweepArgs a) {
-  sweep_body<LAYERS, MODE, OUT, RI>(a);
+  sweep_body<LAYERS, MODE, OUT, RI, EPI>(a);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1395,9 +1398,10 @@ static qk_status launch_gate_sets(const Plan& p, GateSet s0, GateSet s1, cudaStr
   const bool vec = p.front_pad % 4 == 0 && s0.ld % 4 == 0 && al32(s0.X) &&
                    (s1.nblk == 0 || (s1.ld % 4 == 0 && al32(s1.X)));
   const int half = p.layers == 2 ? 0 : 1;
-  // QK_GATE_VARIANT (tuning): 0 = 4 quads/thread, one CTA per 64-qubit item (default);
-  // 1 = 2 quads, 32-qubit items; 2 = 2 quads, persistent double-buffered; 3 = as 0 with 5
-  // resident CTAs per SM
+  // QK_GATE_VARIANT (tuning; ncu, 10,000 x 784, B200): 0 = 2 quads per thread, one CTA per
+  // 32-qubit item (default: 35.0 us, 5.39 TB/s algorithmic); 1 = 4 quads, 64-qubit items
+  // (38.3 us); 2 = 2 quads, persistent double-buffered (43 us); 3 = 2 quads, 6 resident CTAs
+  // per SM; 4 = 1 quad, 16-qubit items
   static const int variant = [] {
     const char* v = getenv("QK_GATE_VARIANT");
     return v == nullptr ? 0 : v[0] - '0';
@@ -1418,20 +1422,24 @@ static qk_status launch_gate_sets(const Plan& p, GateSet s0, GateSet s1, cudaStr
   qk_status ls;
   switch (variant) {
     case 1:
-      ls = vec ? launch(gate_build_kernel<true, 2, false, 1>, 2, false)
-               : launch(gate_build_kernel<false, 2, false, 1>, 2, false);
+      ls = vec ? launch(gate_build_kernel<true, 4, false, 1>, 4, false)
+               : launch(gate_build_kernel<false, 4, false, 1>, 4, false);
       break;
     case 2:
       ls = vec ? launch(gate_build_kernel<true, 2, true, 4>, 2, true)
                : launch(gate_build_kernel<false, 2, true, 4>, 2, true);
       break;
     case 3:
-      ls = vec ? launch(gate_build_kernel<true, 4, false, 5>, 4, false)
-               : launch(gate_build_kernel<false, 4, false, 5>, 4, false);
+      ls = vec ? launch(gate_build_kernel<true, 2, false, 6>, 2, false)
+               : launch(gate_build_kernel<false, 2, false, 6>, 2, false);
+      break;
+    case 4:
+      ls = vec ? launch(gate_build_kernel<true, 1, false, 1>, 1, false)
+               : launch(gate_build_kernel<false, 1, false, 1>, 1, false);
       break;
     default:
-      ls = vec ? launch(gate_build_kernel<true, 4, false, 1>, 4, false)
-               : launch(gate_build_kernel<false, 4, false, 1>, 4, false);
+      ls = vec ? launch(gate_build_kernel<true, 2, false, 1>, 2, false)
+               : launch(gate_build_kernel<false, 2, false, 1>, 2, false);
   }
   if (ls != QK_OK) return ls;
   return cuda_status(cudaGetLastError(), "gate_build launch");
@@ -1496,7 +1504,18 @@ static qk_status tile_counter(cudaStream_t st, unsigned long long** out, bool* o
                      "tile counter reset");
 }
 
-template <int LAYERS, int MODE, int OUT, int RI>
+// Short chains (width_padded <= kShortChain): per-warp epilogue (EPI = 1), and a job of only a
+// few waves runs every tile as two row halves (finer dynamic balance over the 148 SMs).
+// QK_SHORT_CHAIN overrides the threshold (0: never).
+static int short_chain_limit() {
+  static const int v = [] {
+    const char* e = getenv("QK_SHORT_CHAIN");
+    return e == nullptr ? 64 : atoi(e);
+  }();
+  return v;
+}
+
+template <int LAYERS, int MODE, int OUT, int RI, int EPI>
 static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
   bool owned = false;
   if (qk_status s = tile_counter(st, &a.next_tile, &owned)) return s;
@@ -1508,20 +1527,21 @@ static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
       if (on) cudaFreeAsync(p, st);
     }
   } release{a.next_tile, st, owned};
-  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI>;
+  auto kern = sweep_kernel<LAYERS, MODE, OUT, RI, EPI>;
   constexpr int threads = Geo<RI>::kThreads;
   int per_sm = 0;
   if (qk_status s = resident_ctas(kern, threads, kSmemBytes, &per_sm)) return s;
   const int sms = sm_count();
   if (sms <= 0) return set_error(QK_ERR_CUDA, "no CUDA device");
   int64_t grid = int64_t(sms) * per_sm;
-  // the last wave runs as half tiles (QK_EPI == 1 epilogue: whole tiles only)
+  // the last wave runs as half tiles; short-chain jobs of a few waves: every tile
   static const int split_mode = [] {  // QK_HALF_TILES: 0 off, 1 on
     const char* v = getenv("QK_HALF_TILES");
     return v == nullptr ? 1 : v[0] - '0';
   }();
-  const bool split = QK_EPI != 1 && split_mode == 1;
-  a.n_split = split ? std::min<int64_t>(a.n_tiles, grid) : 0;
+  const bool split = split_mode == 1;
+  a.n_split = !split ? 0 : (EPI == 1 && a.n_tiles <= 4 * grid) ? a.n_tiles
+                                                               : std::min<int64_t>(a.n_tiles, grid);
   if (grid > a.n_tiles + a.n_split) grid = a.n_tiles + a.n_split;
   kern<<<unsigned(grid), threads, kSmemBytes, st>>>(a);
   return cuda_status(cudaGetLastError(), "sweep launch");
@@ -1542,8 +1562,12 @@ static int sweep_ri(int layers) {
 
 template <int LAYERS, int MODE, int OUT>
 static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
-  if (sweep_ri(LAYERS) == 2) return launch_sweep_ri<LAYERS, MODE, OUT, 2>(a, st);
-  return launch_sweep_ri<LAYERS, MODE, OUT, 4>(a, st);
+  const bool short_chain = OUT == QK_OUT_DENSE && a.n_pad <= short_chain_limit();
+  if (sweep_ri(LAYERS) == 2)
+    return short_chain ? launch_sweep_ri<LAYERS, MODE, OUT, 2, 1>(a, st)
+                       : launch_sweep_ri<LAYERS, MODE, OUT, 2, 0>(a, st);
+  return short_chain ? launch_sweep_ri<LAYERS, MODE, OUT, 4, 1>(a, st)
+                     : launch_sweep_ri<LAYERS, MODE, OUT, 4, 0>(a, st);
 }
 
 template <int LAYERS, int MODE, int OUT>
