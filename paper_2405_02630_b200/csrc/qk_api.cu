@@ -1,9 +1,11 @@
 // qk_api.cu — C-ABI entry points of libqk: argument validation, launches, and the
 // host-buffer pipelines behind compute_kernel_matrix / compute_cross_kernel.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <thread>
@@ -156,9 +158,34 @@ class CopyPool {
   void touch(void* dst, size_t n) { run(dst, nullptr, n); }
 
  private:
+  // Copies with non-temporal (streaming) stores: the destination lines go to DRAM instead of
+  // sitting dirty in the host's last-level cache.  For the pinned input stage this matters on
+  // the GPU side: a DMA read of cache-resident dirty lines ran at ~25 GB/s instead of ~55
+  // (measured: the config-4 rest upload took 2.8-3.3 ms instead of 1.3 whenever nothing else
+  // had pushed the staged angles out of the 60 MB L3); for the user's output buffers it also
+  // skips the read-for-ownership of every destination line.
+  static void stream_copy(char* d, const char* s, size_t n) {
+    size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+    if (head > n) head = n;
+    std::memcpy(d, s, head);
+    d += head, s += head, n -= head;
+    const size_t v = n / 64;
+    for (size_t k = 0; k < v; ++k, d += 64, s += 64) {
+      const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s));
+      const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 16));
+      const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 32));
+      const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 48));
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d), a);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 16), b);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 32), c);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 48), e);
+    }
+    std::memcpy(d, s, n - v * 64);
+    _mm_sfence();
+  }
   static void work(char* d, const char* sp, size_t lo, size_t hi) {
     if (sp != nullptr) {
-      std::memcpy(d + lo, sp + lo, hi - lo);
+      stream_copy(d + lo, sp + lo, hi - lo);
       return;
     }
     for (size_t o = (lo + 4095) & ~size_t(4095); o < hi; o += 4096)
@@ -463,6 +490,20 @@ struct Trace {
   void mark(int k, cudaStream_t st) {
     if (on) cudaEventRecord(ev[k], st);
   }
+  // named device event (ms after ev[0] on the device) and host timestamp (ms after the trace
+  // started on the host), printed on a second line
+  void point(const char* name, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    pts.push_back({name, e});
+  }
+  void host(const char* name) {
+    if (on)
+      hpts.push_back({name, std::chrono::duration<double, std::milli>(
+                                std::chrono::steady_clock::now() - t0).count()});
+  }
   ~Trace() {
     if (!on) return;
     cudaEventSynchronize(ev[5]);
@@ -470,8 +511,23 @@ struct Trace {
     for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
     fprintf(stderr, "qk_trace h2d %.3f gate %.3f sweep %.3f tail %.3f host %.3f ms\n", t[0],
             t[1], t[2], t[3], t[4]);
+    if (!pts.empty() || !hpts.empty()) {
+      fprintf(stderr, "qk_trace2");
+      for (auto& p : pts) {
+        float ms = 0;
+        cudaEventSynchronize(p.second);
+        cudaEventElapsedTime(&ms, ev[0], p.second);
+        fprintf(stderr, " dev:%s=%.3f", p.first, ms);
+        cudaEventDestroy(p.second);
+      }
+      for (auto& h : hpts) fprintf(stderr, " host:%s=%.3f", h.first, h.second);
+      fprintf(stderr, "\n");
+    }
     for (auto& e : ev) cudaEventDestroy(e);
   }
+  std::vector<std::pair<const char*, cudaEvent_t>> pts;
+  std::vector<std::pair<const char*, double>> hpts;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
 };
 
 template <class Launch>
@@ -521,6 +577,7 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
         copy_pool().touch(tg[k].h_K, size_t(tg[k].n_rows) * tg[k].n_cols * sizeof(double));
   }
   if (trace) trace->mark(3, w->stream);
+  if (trace) trace->host("touched");
   cudaStream_t cs = w->copy_stream;
   if (!all_pinned) {  // the staging slots may still feed the H2D of the inputs
     for (int k = 0; k < 2; ++k)
@@ -649,6 +706,7 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
     }
   }
   if (trace) trace->mark(4, cs);
+  if (trace) trace->host("drain_enqueued");
   cudaError_t e2 = cudaStreamSynchronize(w->stream);
   cudaError_t e3 = cudaStreamSynchronize(cs);
   if (trace) trace->mark(5, cs);
@@ -783,10 +841,10 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
     // The main stream waits for the rest at the end (the drain does not need it: it follows
     // the tile-row counters).
     cudaStream_t hs = w->h2d_stream;
-    cudaEvent_t ev[2];
+    cudaEvent_t ev[2];  // head planes + resets, rest sweep done
     for (int k = 0; k < 2; ++k)
       if (cudaError_t e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming)) {
-        if (k) cudaEventDestroy(ev[0]);
+        for (int j = 0; j < k; ++j) cudaEventDestroy(ev[j]);
         return cuda_err(e, "cudaEventCreate");
       }
     struct Destroy {
@@ -800,6 +858,8 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, 0, n_head, dKt, dKs, st,
                                         tg[0].d_prog, tg[1].d_prog, B))
             return s2;
+          trace.point("head_end", st);
+          trace.host("head_launched");
           if (staged) {  // host copies of the rest while the head sweeps
             cudaStreamQuery(st);  // flush the head launch to the device first
             copy_pool().copy(static_cast<char*>(w->in_stage) + size_t(s1) * row,
@@ -807,11 +867,14 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
             if (n_test > 0)
               copy_pool().copy(const_cast<double*>(src_te), h_test, xsb);
           }
+          trace.host("rest_staged");
+          trace.point("rest_h2d_start", hs);
           cudaError_t e = cudaMemcpyAsync(dXt + s1 * p->width, src_tr + s1 * p->width,
                                           size_t(n_train - s1) * row, cudaMemcpyHostToDevice,
                                           hs);
           if (e == cudaSuccess && n_test > 0)
             e = cudaMemcpyAsync(dXs, src_te, xsb, cudaMemcpyHostToDevice, hs);
+          trace.point("rest_h2d_end", hs);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev[0], 0);  // head planes, resets
           // on a failure past this point, let the rest's queued work finish before returning
           // (it reads and writes the workspace the next call reuses)
@@ -823,9 +886,11 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
           if (qk_status s2 = launch_gate_build2(*p, dXt, n_train, dPt, w->bad, dXs, n_test, dPs,
                                                 w->bad + 1, hs, B))
             return fail(s2);
+          trace.point("rest_sweep_start", hs);
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, hs,
                                         tg[0].d_prog, tg[1].d_prog, B))
             return fail(s2);
+          trace.point("rest_sweep_end", hs);
           e = cudaEventRecord(ev[1], hs);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[1], 0);
           return e == cudaSuccess ? QK_OK : fail(cuda_err(e, "rest sweep join"));

@@ -157,18 +157,80 @@ def _is_cuda_tensor(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
 
+class _HostCache:
+    """Recycles the large anonymous mappings behind result matrices.
+
+    A fresh 960 MB result (config 4) costs page faults on first touch (taken by the copy-out
+    pool while the sweep runs) and ~2 ms of munmap when the caller drops it — on the caller's
+    critical path.  Mappings of dropped results are kept here (up to ``QK_HOST_CACHE_MB``,
+    default 4096; 0 disables) and handed to the next result of the same size, already faulted
+    in.  A result's numpy array holds its mapping through :class:`_Mapping`, whose finaliser
+    runs only once every view of the array is gone."""
+
+    def __init__(self):
+        import os
+        import threading
+
+        self.limit = int(os.environ.get("QK_HOST_CACHE_MB", "4096")) << 20
+        self.free: dict[int, list] = {}
+        self.bytes = 0
+        self.lock = threading.Lock()
+
+    def get(self, nbytes: int):
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                self.bytes -= nbytes
+                return lst.pop()
+        buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        try:
+            buf.madvise(mmap.MADV_HUGEPAGE)
+        except (AttributeError, OSError):  # pragma: no cover - platform without THP advice
+            pass
+        return buf
+
+    def put(self, buf) -> None:
+        n = len(buf)
+        with self.lock:
+            if self.bytes + n <= self.limit:
+                self.free.setdefault(n, []).append(buf)
+                self.bytes += n
+                return
+        buf.close()
+
+
+_host_cache = _HostCache()
+
+
+class _Mapping:
+    """Buffer-protocol owner of one cached mapping (numpy keeps it as the array's base)."""
+
+    __slots__ = ("buf",)
+
+    def __init__(self, buf):
+        self.buf = buf
+
+    def __buffer__(self, flags):
+        return memoryview(self.buf)
+
+    def __release_buffer__(self, view):
+        view.release()
+
+    def __del__(self):
+        cache = _host_cache
+        if cache is not None and self.buf is not None:
+            cache.put(self.buf)
+            self.buf = None
+
+
 def host_empty(shape) -> np.ndarray:
     """Uninitialised float64 host array; large ones are anonymous mappings advised to use
-    transparent huge pages, so the first touch by the copy-out pool faults 2 MB at a time."""
+    transparent huge pages (the first touch by the copy-out pool faults 2 MB at a time),
+    recycled through :class:`_HostCache` once the caller drops them."""
     nbytes = prod(shape) * 8
     if nbytes < (64 << 20):
         return np.empty(shape, dtype=np.float64)
-    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
-    try:
-        buf.madvise(mmap.MADV_HUGEPAGE)
-    except (AttributeError, OSError):  # pragma: no cover - platform without THP advice
-        pass
-    return np.frombuffer(buf, dtype=np.float64).reshape(shape)
+    return np.frombuffer(_Mapping(_host_cache.get(nbytes)), dtype=np.float64).reshape(shape)
 
 
 def _host_angles(x, width: int) -> np.ndarray:

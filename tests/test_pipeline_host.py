@@ -90,3 +90,26 @@ def test_error_hierarchy_matches_reference():
         assert issubclass(cls, TnkernelError)
     err = E.ConvergenceError("cap", alphas=[1], bias=0.5, kkt_residual=1e-3)
     assert err.bias == 0.5
+
+
+def test_host_result_mappings_are_recycled_only_after_every_view_is_gone():
+    from paper_2405_02630_b200.kernel_pipeline import _host_cache, host_empty
+
+    shape = (9000, 1000)  # 72 MB: above the mapping threshold
+    before = _host_cache.bytes
+    a = host_empty(shape)
+    a[:] = 2.0
+    addr = a.ctypes.data
+    view = a[10:20, 5]
+    del a
+    assert _host_cache.bytes == before  # a view still holds the mapping
+    assert float(view[0]) == 2.0
+    del view
+    assert _host_cache.bytes == before + 72_000_000
+    b = host_empty(shape)  # same size: the cached mapping, already faulted in
+    assert b.ctypes.data == addr and b.shape == shape and b.flags.c_contiguous
+    c = host_empty(shape)  # cache empty for this size again: a new mapping
+    assert c.ctypes.data != addr
+    small = host_empty((10, 10))  # small results are plain numpy arrays
+    assert small.base is None or not hasattr(small.base, "__buffer__")
+    del b, c
