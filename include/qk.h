@@ -136,16 +136,20 @@ qk_status qk_job_tiles(const qk_plan* plan, const void* d_planes_train, int64_t 
                        const void* d_planes_test, int64_t n_test, int64_t tile_begin,
                        int64_t tile_end, double* d_K_train, double* d_K_cross, void* stream);
 /* One whole job step on DEVICE angles (train [n_train x width], test [n_test x width], row-
- * major), one host call: both non-finite sentinels reset, the gate planes of both sets
+ * major), one host call: the job state reset (one memset), the gate planes of both sets
  * built in one launch (the rebind of network.py:283-302, per sample), then the joint tile
- * range [tile_begin, tile_end) of qk_job_tiles swept in one persistent launch — the
- * small-job path (stream-ordered, capturable in a CUDA graph).  d_planes_*: caller buffers
- * of qk_planes_bytes(n).  d_bad2: two uint64 sentinels (train, test), valid once the stream
- * has synchronised: UINT64_MAX when every angle is finite, else the first non-finite sample
- * (the caller raises the reference's RebindError, network.py:295-296). */
+ * range [tile_begin, tile_end) of qk_job_tiles swept in one persistent launch that follows
+ * the gate build as a programmatic dependent — the small-job path (stream-ordered,
+ * capturable in a CUDA graph: three nodes).  d_planes_*: caller buffers of
+ * qk_planes_bytes(n).  d_state: QK_JOB_STATE_WORDS uint64 words of device scratch owned by
+ * the caller: [0], [1] = the non-finite sentinels (train, test), valid once the stream has
+ * synchronised: UINT64_MAX when every angle is finite, else the first non-finite sample (the
+ * caller raises the reference's RebindError, network.py:295-296); [2] = the sweep's tile-
+ * claim counter.  Calls sharing one d_state must be stream-ordered. */
+#define QK_JOB_STATE_WORDS 3
 qk_status qk_job_run(const qk_plan* plan, const double* d_train, int64_t n_train,
                      const double* d_test, int64_t n_test, void* d_planes_train,
-                     void* d_planes_test, uint64_t* d_bad2, int64_t tile_begin,
+                     void* d_planes_test, uint64_t* d_state, int64_t tile_begin,
                      int64_t tile_end, double* d_K_train, double* d_K_cross, void* stream);
 /* contract_batch drop-in (engine.py:132-166): signed real amplitudes
  * <0|U(a_p)^dag U(b_q)|0> for an explicit list of index pairs d_pairs[k] = (p, q),

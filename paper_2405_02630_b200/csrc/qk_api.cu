@@ -367,7 +367,7 @@ qk_status qk_unpack_cross(const qk_plan* plan, const double* d_packed, int64_t n
 
 qk_status qk_job_run(const qk_plan* plan, const double* d_train, int64_t n_train,
                      const double* d_test, int64_t n_test, void* d_planes_train,
-                     void* d_planes_test, uint64_t* d_bad2, int64_t tile_begin,
+                     void* d_planes_test, uint64_t* d_state, int64_t tile_begin,
                      int64_t tile_end, double* d_K_train, double* d_K_cross, void* stream) {
   const Plan* p;
   if (qk_status s = check_plan(plan, &p)) return s;
@@ -375,20 +375,24 @@ qk_status qk_job_run(const qk_plan* plan, const double* d_train, int64_t n_train
   if (n_train < 0 || n_test < 0 || tile_begin < 0 || tile_end < tile_begin || tile_end > nt)
     return set_error(QK_ERR_VALUE, "tile range outside the job tile list");
   if (n_train == 0) return QK_OK;
-  if (!d_train || !d_planes_train || !d_bad2 || !d_K_train ||
+  if (!d_train || !d_planes_train || !d_state || !d_K_train ||
       (n_test > 0 && (!d_test || !d_planes_test || !d_K_cross)))
     return set_error(QK_ERR_VALUE, "NULL buffer");
   if (!aligned16(d_planes_train) || (n_test > 0 && !aligned16(d_planes_test)))
     return set_error(QK_ERR_VALUE, "planes must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaError_t e = cudaMemsetAsync(d_bad2, 0xFF, 2 * sizeof(uint64_t), st))
-    return cuda_err(e, "sentinel reset");
-  if (qk_status s = launch_gate_build2(*p, d_train, n_train, d_planes_train, d_bad2, d_test,
-                                       n_test, d_planes_test, d_bad2 + 1, st))
+  // sentinels and the sweep's claim counter (all-ones = no claim yet) in one memset, ahead
+  // of the gate build, so the sweep can follow the gate build as a programmatic dependent
+  // launch (its prologue overlaps the build's tail)
+  if (cudaError_t e = cudaMemsetAsync(d_state, 0xFF, QK_JOB_STATE_WORDS * sizeof(uint64_t), st))
+    return cuda_err(e, "job state reset");
+  if (qk_status s = launch_gate_build2(*p, d_train, n_train, d_planes_train, d_state, d_test,
+                                       n_test, d_planes_test, d_state + 1, st))
     return s;
   if (tile_end == tile_begin) return QK_OK;
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(d_state + 2);
   return launch_job(*p, d_planes_train, n_train, d_planes_test, n_test, tile_begin, tile_end,
-                    d_K_train, d_K_cross, st);
+                    d_K_train, d_K_cross, st, nullptr, nullptr, 0, ctr, true);
 }
 
 qk_status qk_pair_amplitudes(const qk_plan* plan, const void* d_planes_a, int64_t n_a,

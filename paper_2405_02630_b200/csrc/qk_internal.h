@@ -78,7 +78,8 @@ qk_status launch_gate_build2(const Plan& p, const double* d_a, int64_t n_a, void
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress = nullptr, int64_t head_b = 0);
+                       unsigned int* d_progress = nullptr, int64_t head_b = 0,
+                       unsigned long long* counter = nullptr, bool pdl = false);
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
                         int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                         int64_t ld, void* stream);
@@ -93,7 +94,13 @@ enum SweepMode { kModeGram = 0, kModeCross = 1, kModeJob = 2 };
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train = nullptr,
-                     unsigned int* d_prog_cross = nullptr, int64_t head_b = 0);
+                     unsigned int* d_prog_cross = nullptr, int64_t head_b = 0,
+                     unsigned long long* counter = nullptr, bool pdl = false);
+// The dynamic tile schedule's claim counter for one sweep launch, zeroed on `st` (a ring slot,
+// or a stream-ordered allocation under graph capture: *owned, free it after the launch).
+// Callers that reset it (all-ones) ahead of a gate build pass it to launch_job / launch_sweep
+// with pdl.
+qk_status acquire_tile_counter(void* stream, unsigned long long** out, bool* owned);
 
 }  // namespace qk
 

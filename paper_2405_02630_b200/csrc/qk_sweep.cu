@@ -36,12 +36,15 @@ namespace qk {
 
 // Thread layout of a tile: kTX threads along j with kRJ j-samples each; along i, RI
 // i-samples per thread (template parameter: RI = 4 -> 256 threads, RI = 2 -> 512 threads).
+// RI = 1: 512 threads over a 32-row work item (every item a half tile, all 16 warps busy with
+// 1 x 4 micro-tiles; short chains, where 64-row items leave too few waves).
 constexpr int kTX = 16;                 // threads along j
 constexpr int kRJ = kTile / kTX;        // j-samples per thread (4)
 template <int RI>
 struct Geo {
   static constexpr int kRI = RI;
-  static constexpr int kTY = kTile / RI;           // threads along i
+  static constexpr int kRows = RI == 1 ? kTile / 2 : kTile;  // tile rows one item's threads span
+  static constexpr int kTY = kRows / RI;           // threads along i
   static constexpr int kThreads = kTX * kTY;
   static constexpr int kWarps = kThreads / 32;
 };
@@ -86,6 +89,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef QK_SPIN_WAIT  // diagnostic: non-suspending test_wait spin instead of try_wait
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "QK_SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra QK_SPIN_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "QK_WAIT_%=:\n\t"
@@ -103,6 +116,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Timeline instrumentation (diagnostic builds only: -DQK_TIMELINE, tools/timeline_probe.py):
+// thread 0 of each CTA records %globaltimer at kernel entry, after the prologue, and per work
+// item at its start (after the claim barrier), after its first stage landed, after the sweep
+// and after the epilogue.  Read back with qk_timeline_read.
+#ifdef QK_TIMELINE
+#ifdef QK_TL_GLOBALTIMER
+#define QK_TL_CLOCK() ([] { unsigned long long v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v)); return v; }())
+#else  // SM cycle counter (cheap; intra-CTA intervals), converted at the nominal clock
+#define QK_TL_CLOCK() ((unsigned long long)clock64())
+#endif
+constexpr int kTLSlots = 256;  // per CTA: 2 + 4 per item (first 23 items), 96 + k: item k issued,
+                               // 128 + k: item k's first stage already full at its start, 160 + k: released,
+                               // 192 + k: warp 0 idle in item k
+__device__ unsigned long long qk_tl_buf[1024 * kTLSlots];
+__device__ __forceinline__ void tl_store(int slot, unsigned long long v) {
+  if (slot < kTLSlots && blockIdx.x < 1024) qk_tl_buf[blockIdx.x * kTLSlots + slot] = v;
+}
+__device__ __forceinline__ void tl_mark(int slot) {
+  if (threadIdx.x == 0 && slot < kTLSlots && blockIdx.x < 1024) {
+    unsigned long long t;
+    t = QK_TL_CLOCK();
+    qk_tl_buf[blockIdx.x * kTLSlots + slot] = t;
+  }
+}
+__device__ __forceinline__ void tl_mark_any(int slot) {  // any thread (e.g. a stage refill)
+  if (slot < kTLSlots && blockIdx.x < 1024) {
+    unsigned long long t;
+    t = QK_TL_CLOCK();
+    qk_tl_buf[blockIdx.x * kTLSlots + slot] = t;
+  }
+}
+#define QK_TL(slot) tl_mark(slot)
+#define QK_TL_ANY(slot) tl_mark_any(slot)
+#else
+#define QK_TL(slot) ((void)0)
+#define QK_TL_ANY(slot) ((void)0)
+#endif
 
 // ------------------------------------------------------------------------------------------
 // The per-qubit recurrences (shared by the tile sweep and the pair-list kernel so the two
@@ -631,6 +682,9 @@ __device__ __forceinline__ void gate_store(const GateItem& g, int n_pad, int hal
 template <bool VEC, int QD, bool PERSIST, int MINB>
 __global__ void __launch_bounds__(256, MINB) gate_build_kernel(GateSet s0, GateSet s1, int width,
                                                                int n_pad, int front, int half) {
+  // a sweep launched behind this kernel as a programmatic dependent may start its prologue
+  // now (it waits for this grid's completion before reading the planes)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int slabs = (n_pad + 16 * QD - 1) / (16 * QD);
   const int64_t n_items = (s0.nblk + s1.nblk) * slabs;
   int64_t it = blockIdx.x;
@@ -692,9 +746,10 @@ struct SweepArgs {
   double* out2;
   unsigned int* progress2;
   int pad_rows, pad_cols, pad_rows2;  // sample_pad() of each plane set (front of block 0)
-  unsigned long long* next_tile;  // dynamic tile claims beyond the first wave (zeroed per launch)
+  unsigned long long* next_tile;  // dynamic tile claims (all-ones before a launch's first claim)
   int64_t n_split;  // the last n_split tiles run as two row halves each (finer last wave)
   int64_t head_b;   // Gram tile order with a B-block head (decode_gram; 0: decode_upper)
+  int pdl;          // host only: launch as a programmatic dependent of the preceding kernel
 };
 
 // Per-tile coordinates: tile rows/cols in plane blocks and which problem of a kModeJob launch.
@@ -727,24 +782,35 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
   const int tid = threadIdx.x;
   const int lane = tid % 32;
   const int nchunks = a.nchunks;
+  QK_TL(0);
 
-  // Dynamic tile schedule: CTA b starts with tile b; every further tile is claimed from a
-  // launch-wide counter (tiles gridDim.x, gridDim.x + 1, ... in list order), so CTAs that
-  // spend time elsewhere (plane builds, cheaper padding tiles) simply take fewer tiles.  The
-  // chunks of a CTA's tile k + kLook are issued during tile k, so tile k + kLook is claimed
-  // (thread 0) at the start of tile k and published by a CTA barrier.  Claims live in a small
-  // shared ring indexed by the CTA-local tile number.
+  // Dynamic tile schedule: CTA b starts with tiles b, b + G, ..., b + kLook G (G = gridDim.x,
+  // static: no atomic in the prologue); every further tile is claimed from a launch-wide
+  // counter (tiles (kLook + 1) G, (kLook + 1) G + 1, ... in list order), so CTAs that spend
+  // time elsewhere (plane builds, cheaper padding tiles) simply take fewer tiles.  The chunks
+  // of a CTA's tile k + kLook are issued during tile k, so tile k + kLook is claimed (thread
+  // 0) at the start of tile k and published by a CTA barrier.  Short chains (RI = 1, a tile of
+  // a few microseconds) issue that claim's atomic one tile earlier and only decode it at the
+  // next tile start, so its latency never stalls the CTA.  Claims live in a small shared ring
+  // indexed by the CTA-local tile number.
   const int kLook = 1 + (kStages - 1) / nchunks;
+  constexpr bool kEarly = RI == 1;
   __shared__ Claim ring[8];
   double* stage_T = reinterpret_cast<double*>(released + 2 * kStages);  // epilogue staging tile
   // Work items: tiles [0, n_tiles - n_split) whole, then the last n_split tiles as two row
   // halves each, so the final wave ends in half-tile steps (a half tile takes about half the
   // time: the warps of the other half skip the sweep like padding rows do).
   const int64_t n_whole = a.n_tiles - a.n_split, n_items = a.n_tiles + a.n_split;
-  auto claim = [&](int64_t k) {  // thread 0 only
+  auto claim_raw = [&](int64_t k) -> int64_t {  // thread 0 only
+    if constexpr (RI == 1)  // the first kLook + 1 tiles static (no atomic in the prologue)
+      return k <= kLook ? int64_t(blockIdx.x) + k * int64_t(gridDim.x)
+                        : (kLook + 1) * int64_t(gridDim.x) + int64_t(atomicAdd(a.next_tile, 1ull) + 1);
+    return k == 0 ? int64_t(blockIdx.x)
+                  : int64_t(gridDim.x) + int64_t(atomicAdd(a.next_tile, 1ull) + 1);
+  };
+  auto claim_set = [&](int64_t k, int64_t g_item) {  // thread 0 only
     Claim c;
-    c.g = k == 0 ? int64_t(blockIdx.x)
-                 : int64_t(gridDim.x) + int64_t(atomicAdd(a.next_tile, 1ull));
+    c.g = g_item;
     c.bi = c.bj = c.prob = 0;
     c.half = -1;
     c.t = c.g;
@@ -769,13 +835,22 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
     ring[k & 7] = c;
   };
   auto valid = [&](int64_t k) { return ring[k & 7].g < n_items; };
+  int64_t pending = 0;  // kEarly: raw claim of tile k + kLook + 1, issued during tile k
   auto tile_of = [&](int64_t k) -> TileXY {
     const Claim& c = ring[k & 7];
     return TileXY{c.bi, c.bj, c.prob};
   };
-  if (tid == 0)
-    for (int64_t k = 0; k <= kLook; ++k) claim(k);
-  __syncthreads();
+  if (tid == 0) {
+    for (int64_t k = 0; k <= kLook; ++k) claim_set(k, claim_raw(k));
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  // Programmatic dependent launch: everything above overlaps the tail of the kernel this one
+  // was launched behind (the gate build); global memory is touched only after this wait.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   auto issue = [&](int64_t f) {  // fill stage f % kStages with item f (if its tile exists)
     const int64_t k = f / nchunks;
     if (!valid(k)) return;
@@ -786,39 +861,47 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
     const double2* si =
         (t.prob ? a.rows2 : a.rows) + (t.bi * a.n_pad + int64_t(c) * kChunk) * kTile;
     const double2* sj = a.cols + (t.bj * a.n_pad + int64_t(c) * kChunk) * kTile;
+    if (c == 0 && k < 32) QK_TL_ANY(96 + int(k));
     mbar_arrive_expect_tx(&full[stage], 2 * kChunkBytes);
     bulk_g2s(dst, si, kChunkBytes, &full[stage]);
     bulk_g2s(dst + kChunkElems, sj, kChunkBytes, &full[stage]);
   };
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      released[s] = 0;
-    }
-    fence_mbar_init();
     for (int64_t f = 0; f < kStages; ++f) issue(f);
+    if (kEarly) pending = claim_raw(kLook + 1);
   }
   __syncthreads();
+  QK_TL(1);
 
   // ---------------- compute warps ----------------
-  // Thread (ty, tx) owns tile rows ty*kRI .. ty*kRI+kRI-1 (consecutive, so a warp covers
-  // 2*kRI whole rows) and columns tx + kTX*c.
+  // Thread (ty, tx) owns tile rows rb + ty*kRI .. rb + ty*kRI+kRI-1 (consecutive, so a warp
+  // covers 2*kRI whole rows) and columns tx + kTX*c; rb = 0, or the item's first row for RI = 1.
   const int tx = tid % kTX, ty = tid / kTX;
-  const int warp_row_end = (tid / 32 + 1) * (32 / kTX) * kRI;  // rows [.., end) of this warp
+  const int warp_row_end0 = (tid / 32 + 1) * (32 / kTX) * kRI;  // rows [.., end) of the warp
   St st[kRI][kRJ];
   int64_t f = 0;
   for (int64_t k = 0; valid(k); ++k) {
     if (k > 0) {  // claim tile k + kLook (its chunks are issued during tile k)
-      if (tid == 0) claim(k + kLook);
+      if (tid == 0) {
+        if (kEarly) {
+          claim_set(k + kLook, pending);
+          pending = claim_raw(k + kLook + 1);
+        } else {
+          claim_set(k + kLook, claim_raw(k + kLook));
+        }
+      }
       __syncthreads();
     }
+    QK_TL(2 + 4 * int(k));
     const TileXY tk = tile_of(k);
     // padding rows of this tile (front of plane block 0): warps made only of them skip the
     // sweep (they still release every stage) — the ragged sample block costs ~1/4 of a tile
     const int pad_r = tk.bi == 0 ? (tk.prob ? a.pad_rows2 : a.pad_rows) : 0;
     const int half = ring[k & 7].half;
     const int r_lo = half == 1 ? kTile / 2 : 0, r_hi = half == 0 ? kTile / 2 : kTile;
+    const int rb = RI == 1 ? r_lo : 0;  // first tile row of this thread layout
+    const int warp_row_end = rb + warp_row_end0;
     const bool idle = warp_row_end <= (pad_r > r_lo ? pad_r : r_lo) ||
                       warp_row_end - (32 / kTX) * kRI >= r_hi;
 #pragma unroll
@@ -828,13 +911,24 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
 
     for (int ch = 0; ch < nchunks; ++ch, ++f) {
       const int stage = int(f % kStages);
+#ifdef QK_TIMELINE
+      if (ch == 0 && tid == 0 && k < 32) {
+        uint32_t ready;
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n}" : "=r"(ready) : "r"(smem_u32(&full[stage])),
+                     "r"(uint32_t((f / kStages) & 1)) : "memory");
+        tl_store(128 + int(k), ready + 1);
+        tl_store(192 + int(k), idle ? 2 : 1);
+      }
+#endif
       mbar_wait(&full[stage], uint32_t((f / kStages) & 1));
+      if (ch == 0) QK_TL(3 + 4 * int(k));
       const double2* sI = sbuf + size_t(stage) * 2 * kChunkElems;
       const double2* sJ = sI + kChunkElems;
       auto qubit = [&](int q) {
         double2 vi[kRI], vj[kRJ];
 #pragma unroll
-        for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + ty * kRI + r];
+        for (int r = 0; r < kRI; ++r) vi[r] = sI[q * kTile + rb + ty * kRI + r];
 #pragma unroll
         for (int c = 0; c < kRJ; ++c) vj[c] = sJ[q * kTile + tx + kTX * c];
         if constexpr (LAYERS == 2 && QK_MT != 0) {
@@ -859,6 +953,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       if (lane == 0) {
         // the last warp to release the stage refills it with item f + kStages
         if (atomicAdd(&released[stage], 1) == kWarps - 1) {
+          if (ch == 0 && k < 32) QK_TL_ANY(160 + int(k));
           released[stage] = 0;
           issue(f + kStages);
         }
@@ -872,6 +967,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
     }
 
     // ---- epilogue ----
+    QK_TL(4 + 4 * int(k));
     const TileXY t = tk;
     const int64_t bi = t.bi, bj = t.bj;
     const bool gram = MODE == kModeGram || (MODE == kModeJob && t.prob == 0);
@@ -881,8 +977,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       for (int r = 0; r < kRI; ++r)
 #pragma unroll
         for (int c = 0; c < kRJ; ++c)
-          if (ty * kRI + r >= r_lo && ty * kRI + r < r_hi)
-            o[(ty * kRI + r) * kTile + tx + kTX * c] =
+          if (rb + ty * kRI + r >= r_lo && rb + ty * kRI + r < r_hi)
+            o[(rb + ty * kRI + r) * kTile + tx + kTX * c] =
                 kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
     } else if (EPI == 1) {
       // Per-warp epilogue, no CTA barrier: the warp's 2*kRI rows go out straight from the
@@ -903,7 +999,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
 #pragma unroll
         for (int c = 0; c < kRJ; ++c) {
           v[r][c] = kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
-          const int64_t i = i0 + ty * kRI + r, j = j0 + tx + kTX * c;
+          const int64_t i = i0 + rb + ty * kRI + r, j = j0 + tx + kTX * c;
           if (!mine) {
           } else if (gram) {
             if (i >= 0 && i < n_rows && j < n_rows && i <= j)
@@ -912,7 +1008,11 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
             out[i * ld + j] = v[r][c];
           }
         }
+#ifdef QK_DIAG_NO_MIRROR  // diagnostic timing variant: the per-warp epilogue skips the mirror
+      if (false) {
+#else
       if (gram && mine) {
+#endif
         const int w = tid / 32;
         double* wb = stage_T + w * (kWR * (kTile + 1));
         __syncwarp();  // this warp's mirror pass of the previous tile has read wb
@@ -922,7 +1022,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
           for (int c = 0; c < kRJ; ++c)
             wb[((ty & 1) * kRI + r) * (kTile + 1) + tx + kTX * c] = v[r][c];
         __syncwarp();
-        const int64_t iw = i0 + w * kWR;  // first row of this warp
+        const int64_t iw = i0 + rb + w * kWR;  // first row of this warp
 #pragma unroll
         for (int h = 0; h < kTile / 32; ++h) {
           const int jl = lane + 32 * h;
@@ -945,7 +1045,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       for (int r = 0; r < kRI; ++r)
 #pragma unroll
         for (int c = 0; c < kRJ; ++c)
-          stage_T[(ty * kRI + r) * (kTile + 1) + tx + kTX * c] =
+          stage_T[(rb + ty * kRI + r) * (kTile + 1) + tx + kTX * c] =
               kernel_value(st_amp<LAYERS>(st[r][c], a.final_scale), a.convention);
       __syncthreads();
       double* out = t.prob ? a.out2 : a.out;
@@ -979,6 +1079,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       __syncthreads();
       if (tid == 0) atomicAdd(prog + bi, half < 0 ? 2u : 1u);  // per tile row: 2 per tile
     }
+    QK_TL(5 + 4 * int(k));
   }
 }
 
@@ -1471,12 +1572,13 @@ qk_status launch_gate_build2(const Plan& p, const double* d_a, int64_t n_a, void
                           static_cast<cudaStream_t>(stream));
 }
 
-// Per-launch tile-claim counters (the dynamic schedule): a ring of zeroed 8-byte slots per
+// Per-launch tile-claim counters (the dynamic schedule): a ring of reset 8-byte slots per
 // device, one per launch, so concurrent launches on different streams never share one.  A
 // launch captured into a CUDA graph gets its own stream-ordered allocation instead (a graph
 // memory node, allocated and freed around the kernel on every replay), so a replay never
 // shares a counter with a later ring launch.  *owned: the caller frees it after the launch.
-static qk_status tile_counter(cudaStream_t st, unsigned long long** out, bool* owned) {
+qk_status acquire_tile_counter(void* stream, unsigned long long** out, bool* owned) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   constexpr int kSlots = 4096;
   static unsigned long long* pool[64] = {};
   static std::mutex mu;
@@ -1500,7 +1602,8 @@ static qk_status tile_counter(cudaStream_t st, unsigned long long** out, bool* o
     }
     *out = pool[dev] + (seq.fetch_add(1) % kSlots);
   }
-  return cuda_status(cudaMemsetAsync(*out, 0, sizeof(unsigned long long), st),
+  // all-ones: a claim adds one and wraps to 0 (one memset value for a job's whole state)
+  return cuda_status(cudaMemsetAsync(*out, 0xFF, sizeof(unsigned long long), st),
                      "tile counter reset");
 }
 
@@ -1517,8 +1620,9 @@ static int short_chain_limit() {
 
 template <int LAYERS, int MODE, int OUT, int RI, int EPI>
 static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
-  bool owned = false;
-  if (qk_status s = tile_counter(st, &a.next_tile, &owned)) return s;
+  bool owned = false;  // a.next_tile preset: the caller reset it earlier in stream order
+  if (a.next_tile == nullptr)
+    if (qk_status s = acquire_tile_counter(st, &a.next_tile, &owned)) return s;
   struct Release {  // a captured counter is freed after the launch, on the same stream
     unsigned long long* p;
     cudaStream_t st;
@@ -1540,11 +1644,34 @@ static qk_status launch_sweep_ri(SweepArgs a, cudaStream_t st) {
     return v == nullptr ? 1 : v[0] - '0';
   }();
   const bool split = split_mode == 1;
-  a.n_split = !split ? 0 : (EPI == 1 && a.n_tiles <= 4 * grid) ? a.n_tiles
-                                                               : std::min<int64_t>(a.n_tiles, grid);
+  static const double split_waves = [] {  // QK_SPLIT_WAVES: tail tiles split, in grids (tuning)
+    const char* v = getenv("QK_SPLIT_WAVES");
+    return v == nullptr ? -1.0 : atof(v);
+  }();
+  if (RI == 1)  // 32-row layout: every item is a half tile
+    a.n_split = a.n_tiles;
+  else if (!split)
+    a.n_split = 0;
+  else if (split_waves >= 0)
+    a.n_split = std::min<int64_t>(a.n_tiles, int64_t(split_waves * grid));
+  else
+    a.n_split = (EPI == 1 && a.n_tiles <= 4 * grid) ? a.n_tiles : std::min<int64_t>(a.n_tiles, grid);
   if (grid > a.n_tiles + a.n_split) grid = a.n_tiles + a.n_split;
-  kern<<<unsigned(grid), threads, kSmemBytes, st>>>(a);
-  return cuda_status(cudaGetLastError(), "sweep launch");
+  if (!a.pdl) {
+    kern<<<unsigned(grid), threads, kSmemBytes, st>>>(a);
+    return cuda_status(cudaGetLastError(), "sweep launch");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, a), "sweep launch (programmatic)");
 }
 
 // Micro-tile rows per thread: 2 (512 threads, 2x4 micro-tiles, 16 warps/SM) or 4 (256
@@ -1560,9 +1687,21 @@ static int sweep_ri(int layers) {
   return layers == 1 ? 4 : 2;
 }
 
+// Short chains at L = 2 run 32-row items with all 16 warps busy (RI = 1) unless
+// QK_SHORT_RI1=0 (then 64-row items, half of them split, with RI = 2).
+static bool short_ri1() {
+  static const bool v = [] {
+    const char* e = getenv("QK_SHORT_RI1");
+    return e == nullptr || e[0] != '0';
+  }();
+  return v;
+}
+
 template <int LAYERS, int MODE, int OUT>
 static qk_status launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   const bool short_chain = OUT == QK_OUT_DENSE && a.n_pad <= short_chain_limit();
+  if constexpr (LAYERS == 2 && OUT == QK_OUT_DENSE)
+    if (short_chain && short_ri1()) return launch_sweep_ri<LAYERS, MODE, OUT, 1, 1>(a, st);
   if (sweep_ri(LAYERS) == 2)
     return short_chain ? launch_sweep_ri<LAYERS, MODE, OUT, 2, 1>(a, st)
                        : launch_sweep_ri<LAYERS, MODE, OUT, 2, 0>(a, st);
@@ -1625,11 +1764,14 @@ static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, 
 qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_rows,
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
-                       unsigned int* d_progress, int64_t head_b) {
+                       unsigned int* d_progress, int64_t head_b, unsigned long long* counter,
+                       bool pdl) {
   if (tile_end <= tile_begin) return QK_OK;
   if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
     return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
   SweepArgs a{};
+  a.next_tile = counter;
+  a.pdl = pdl ? 1 : 0;
   if (mode == kModeGram) a.head_b = head_b;
   a.progress = d_progress;
   a.rows = static_cast<const double2*>(d_rows);
@@ -1689,7 +1831,8 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
 qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const void* d_test,
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train,
-                     unsigned int* d_prog_cross, int64_t head_b) {
+                     unsigned int* d_prog_cross, int64_t head_b, unsigned long long* counter,
+                     bool pdl) {
   if (tile_end <= tile_begin) return QK_OK;
   if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
     return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
@@ -1697,16 +1840,22 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
   const int64_t n_gram = nbt * (nbt + 1) / 2;
   if (p.layers >= 3 || n_test == 0 || tile_end <= n_gram || tile_begin >= n_gram) {
     // one problem only (or the one-pair-per-thread L >= 3 kernel): plain launches
+    // (the caller's counter and programmatic launch go to the Gram launch, or to the cross
+    // launch when the range holds no Gram tile)
+    const bool gram_first = tile_begin < std::min(tile_end, n_gram);
     if (qk_status s = launch_sweep(p, kModeGram, d_train, n_train, d_train, n_train, tile_begin,
                                    std::min(tile_end, n_gram), d_K_train, n_train,
-                                   QK_OUT_DENSE, stream, d_prog_train, head_b))
+                                   QK_OUT_DENSE, stream, d_prog_train, head_b, counter, pdl))
       return s;
     if (n_test == 0 || tile_end <= n_gram) return QK_OK;
     return launch_sweep(p, kModeCross, d_test, n_test, d_train, n_train,
                         std::max(tile_begin, n_gram) - n_gram, tile_end - n_gram, d_K_cross,
-                        n_train, QK_OUT_DENSE, stream, d_prog_cross);
+                        n_train, QK_OUT_DENSE, stream, d_prog_cross, 0,
+                        gram_first ? nullptr : counter, !gram_first && pdl);
   }
   SweepArgs a{};
+  a.next_tile = counter;
+  a.pdl = pdl ? 1 : 0;
   a.head_b = head_b;
   a.rows = static_cast<const double2*>(d_train);
   a.cols = static_cast<const double2*>(d_train);
@@ -1816,3 +1965,16 @@ qk_status launch_dfma_peak(double* out, void* stream) {
 }
 
 }  // namespace qk
+
+#ifdef QK_TIMELINE
+extern "C" int qk_timeline_read(unsigned long long* host, int n_ctas, int clear) {
+  const size_t bytes = size_t(n_ctas) * qk::kTLSlots * sizeof(unsigned long long);
+  if (cudaMemcpyFromSymbol(host, qk::qk_tl_buf, bytes) != cudaSuccess) return 5;
+  if (clear) {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, qk::qk_tl_buf);
+    cudaMemset(p, 0, sizeof(unsigned long long) * 1024 * qk::kTLSlots);
+  }
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -375,7 +375,8 @@ class KernelJob:
         self.K_train = None
         self.K_cross = None
         self._shared = None
-        self._bad = None             # [2] int64 non-finite sentinels (train, test)
+        self._bad = None             # [3] int64 job state: non-finite sentinels (train, test),
+                                     # qk_job_run's tile-claim counter
         self._planes = [None, None]  # gate-plane buffers reused across runs
         self._g = None               # captured single-GPU job (small jobs)
 
@@ -512,7 +513,7 @@ class KernelJob:
             return self.K_train, self.K_cross
         devc = train_angles.device
         if self._bad is None or self._bad.device != devc:
-            self._bad = torch.empty(2, dtype=torch.int64, device=devc)
+            self._bad = torch.empty(3, dtype=torch.int64, device=devc)
             self._planes = [None, None]
         self._bad.fill_(-1)  # both plane sets' non-finite sentinels, one fill
         p_train = dev.gate_build(self.plan, train_angles, out=self._planes[0],
@@ -540,7 +541,7 @@ class KernelJob:
             return bool(mode)
         return self.layout.entries() * self.plan.width <= self.GRAPH_ENTRY_QUBITS
 
-    def _run_graph(self, train_angles, test_angles) -> None:
+    def _check_job_inputs(self, train_angles, test_angles) -> None:
         from . import device as dev
 
         lay, plan = self.layout, self.plan
@@ -553,39 +554,58 @@ class KernelJob:
                               f"{tuple(train_angles.shape)} / "
                               f"{tuple(test_angles.shape) if lay.n_test else ()} do not match "
                               f"the job ({lay.n_train}, {lay.n_test}) x width {plan.width}")
+
+    def _ensure_job_buffers(self, devc) -> None:
+        """Job-owned device buffers of the single-GPU qk_job_run path: both plane sets, the
+        job state (sentinels + tile-claim counter) and the two matrices."""
+        if getattr(self, "_jb_dev", None) == devc:
+            return
+        lay, plan = self.layout, self.plan
+        f64 = dict(dtype=torch.float64, device=devc)
+        self._g_planes = [torch.empty(max(plan.planes_bytes(n), 16), dtype=torch.uint8,
+                                      device=devc) for n in (lay.n_train, lay.n_test)]
+        self._bad = torch.empty(3, dtype=torch.int64, device=devc)  # QK_JOB_STATE_WORDS
+        self.K_train = torch.empty((lay.n_train, lay.n_train), **f64)
+        self.K_cross = torch.empty((lay.n_test, lay.n_train), **f64) if lay.n_test else None
+        self._nt = int(_native.lib().qk_job_tile_count(plan.handle, lay.n_train, lay.n_test))
+        self._g = None
+        self._jb_dev = devc
+
+    def _job_run_call(self, train_ptr: int, test_ptr: int | None) -> None:
+        """One qk_job_run on the current stream: state reset, both gate builds in one launch,
+        the sweep as a programmatic dependent of the build (three graph nodes when captured)."""
+        from . import device as dev
+
+        lay = self.layout
+        _native.check(_native.lib().qk_job_run(
+            self.plan.handle, train_ptr, lay.n_train, test_ptr if lay.n_test else None,
+            lay.n_test, self._g_planes[0].data_ptr(),
+            self._g_planes[1].data_ptr() if lay.n_test else None, self._bad.data_ptr(), 0,
+            self._nt, self.K_train.data_ptr(),
+            self.K_cross.data_ptr() if lay.n_test else None, dev._stream()))
+
+    def _capture_job(self, train_ptr: int, test_ptr: int | None, devc):
+        side = torch.cuda.Stream(device=devc)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._job_run_call(train_ptr, test_ptr)  # first use (launch caches), uncaptured
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._job_run_call(train_ptr, test_ptr)
+        return g
+
+    def _run_graph(self, train_angles, test_angles) -> None:
+        lay, plan = self.layout, self.plan
+        self._check_job_inputs(train_angles, test_angles)
         devc = train_angles.device
-        if self._g is None or self._g_dev != devc:
+        self._ensure_job_buffers(devc)
+        if self._g is None:
             f64 = dict(dtype=torch.float64, device=devc)
-            self._g_in = [torch.empty((lay.n_train, plan.width), **f64),
-                          torch.empty((max(lay.n_test, 1), plan.width), **f64)]
-            self._g_planes = [torch.empty(max(plan.planes_bytes(n), 16), dtype=torch.uint8,
-                                          device=devc) for n in (lay.n_train, lay.n_test)]
-            self._bad = torch.empty(2, dtype=torch.int64, device=devc)
-            self.K_train = torch.empty((lay.n_train, lay.n_train), **f64)
-            self.K_cross = torch.empty((lay.n_test, lay.n_train), **f64) if lay.n_test else None
-            lib = _native.lib()
-            nt = int(lib.qk_job_tile_count(plan.handle, lay.n_train, lay.n_test))
-
-            def body():
-                _native.check(lib.qk_job_run(
-                    plan.handle, self._g_in[0].data_ptr(), lay.n_train,
-                    self._g_in[1].data_ptr() if lay.n_test else None, lay.n_test,
-                    self._g_planes[0].data_ptr(),
-                    self._g_planes[1].data_ptr() if lay.n_test else None,
-                    self._bad.data_ptr(), 0, nt, self.K_train.data_ptr(),
-                    self.K_cross.data_ptr() if lay.n_test else None, dev._stream()))
-
-            side = torch.cuda.Stream(device=devc)
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                self._g_in[0].zero_()
-                self._g_in[1].zero_()
-                body()  # first use (launch caches), uncaptured
-            torch.cuda.current_stream().wait_stream(side)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                body()
-            self._g, self._g_dev = g, devc
+            self._g_in = [torch.zeros((lay.n_train, plan.width), **f64),
+                          torch.zeros((max(lay.n_test, 1), plan.width), **f64)]
+            self._g = self._capture_job(self._g_in[0].data_ptr(), self._g_in[1].data_ptr(),
+                                        devc)
         self._g_in[0].copy_(train_angles)
         if lay.n_test:
             self._g_in[1].copy_(test_angles)
@@ -595,7 +615,7 @@ class KernelJob:
         """The reference's RebindError for a non-finite angle (network.py:295-296), indexed
         like the single-process API: the first Gram pair (row-major) holding a
         bad train sample, else the first cross pair holding a bad test sample."""
-        bad_train, bad_test = self._bad.tolist()  # one device sync for both sentinels
+        bad_train, bad_test = self._bad[:2].tolist()  # one device sync for both sentinels
         if bad_train != -1:
             raise RebindError(f"operand set {0 if bad_train == 0 else bad_train - 1}: feature "
                               "angles must be finite")
@@ -604,24 +624,23 @@ class KernelJob:
                               "must be finite")
 
     def graph(self, train_angles: torch.Tensor, test_angles: torch.Tensor | None = None):
-        """CUDA-graph capture of :meth:`run` (world size 1): returns ``(replay, K_train,
+        """CUDA-graph capture of one job step (world size 1): returns ``(replay, K_train,
         K_cross)``; ``replay()`` recomputes both matrices into the same tensors from the
-        current contents of ``train_angles`` / ``test_angles`` with one graph launch — for
-        small jobs repeated many times (below ~64 qubits the per-call host work of ``run``,
-        ~0.05 ms, is comparable with the sweep itself)."""
+        current contents of ``train_angles`` / ``test_angles`` with one graph launch (the
+        captured qk_job_run: state reset, gate build, sweep) — for small jobs repeated many
+        times (below ~64 qubits the per-call host work of ``run``, ~0.05 ms, is comparable
+        with the sweep itself).  Non-finite angles are not checked on replay: the sentinels
+        are in ``self._bad[:2]`` (see :meth:`run`)."""
         if self.world != 1:
             raise ValueError("graph capture is single-process (the multi-rank job synchronises "
                              "ranks between launches)")
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            self.run(train_angles, test_angles)  # allocations and first-use setup, uncaptured
-        torch.cuda.current_stream().wait_stream(side)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            K, Kx = self.run(train_angles, test_angles)
-        self._graph = g  # keeps the graph (and its memory pool) alive with the job
-        return g.replay, K, Kx
+        self._check_job_inputs(train_angles, test_angles)
+        devc = train_angles.device
+        self._ensure_job_buffers(devc)
+        g = self._capture_job(train_angles.data_ptr(),
+                              test_angles.data_ptr() if self.layout.n_test else None, devc)
+        self._graph = g  # keeps the graph alive with the job
+        return g.replay, self.K_train, self.K_cross
 
     # ---- host buffers in and out ----------------------------------------------------------
     def host_outputs(self) -> tuple:

@@ -20,7 +20,7 @@ def case(n, n_a, n_b, reps=20):
     B = torch.as_tensor(rng.uniform(0, np.pi, (max(n_b, 1), n)), device="cuda")
     pa = torch.empty(plan.planes_bytes(n_a), dtype=torch.uint8, device="cuda")
     pb = torch.empty(max(plan.planes_bytes(n_b), 16), dtype=torch.uint8, device="cuda")
-    bad = torch.full((2,), -1, dtype=torch.int64, device="cuda")
+    bad = torch.full((3,), -1, dtype=torch.int64, device="cuda")
     Ktr = torch.empty((1, 1), dtype=torch.float64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     lib = _native.lib()
