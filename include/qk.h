@@ -157,6 +157,12 @@ qk_status qk_job_run(const qk_plan* plan, const double* d_train, int64_t n_train
 qk_status qk_pair_amplitudes(const qk_plan* plan, const void* d_planes_a, int64_t n_a,
                              const void* d_planes_b, int64_t n_b, const int64_t* d_pairs,
                              int64_t n_pairs, double* d_amp, void* stream);
+/* The same pairs as kernel values K(a_p, b_q) under the plan's convention (|amp|^2 or |amp|,
+ * statevector.py:62-70) — the SPEC's `--shard k/W` partial:
+ * one value per strict-upper or cross pair, in input order.  Out-of-range indices give NaN. */
+qk_status qk_pair_kernel_values(const qk_plan* plan, const void* d_planes_a, int64_t n_a,
+                                const void* d_planes_b, int64_t n_b, const int64_t* d_pairs,
+                                int64_t n_pairs, double* d_K, void* stream);
 
 /* ---- host-buffer entry points (the user-facing call; synchronous) ----------------
  * compute_kernel_matrix and compute_cross_kernel

@@ -59,6 +59,8 @@ _SIGNATURES = {
                                        _c_i64, _c_vp]),
     "qk_pair_amplitudes": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_i64,
                                           _c_vp, _c_vp]),
+    "qk_pair_kernel_values": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp,
+                                             _c_i64, _c_vp, _c_vp]),
     "qk_kernel_matrix_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp]),
     "qk_cross_kernel_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp]),
     "qk_dfma_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), _c_vp]),

@@ -407,6 +407,17 @@ qk_status qk_pair_amplitudes(const qk_plan* plan, const void* d_planes_a, int64_
   return launch_pairs(*p, d_planes_a, n_a, d_planes_b, n_b, d_pairs, n_pairs, d_amp, stream);
 }
 
+qk_status qk_pair_kernel_values(const qk_plan* plan, const void* d_planes_a, int64_t n_a,
+                                const void* d_planes_b, int64_t n_b, const int64_t* d_pairs,
+                                int64_t n_pairs, double* d_K, void* stream) {
+  const Plan* p;
+  if (qk_status s = check_plan(plan, &p)) return s;
+  if (n_pairs < 0 || n_a < 0 || n_b < 0) return set_error(QK_ERR_VALUE, "negative size");
+  if (n_pairs == 0) return QK_OK;
+  if (!d_planes_a || !d_planes_b || !d_pairs || !d_K) return set_error(QK_ERR_VALUE, "NULL buffer");
+  return launch_pairs(*p, d_planes_a, n_a, d_planes_b, n_b, d_pairs, n_pairs, d_K, stream, true);
+}
+
 qk_status qk_dfma_peak(double* out_flops_per_s, void* stream) {
   if (out_flops_per_s == nullptr) return set_error(QK_ERR_VALUE, "NULL output");
   return launch_dfma_peak(out_flops_per_s, stream);

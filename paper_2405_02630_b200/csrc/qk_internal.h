@@ -83,8 +83,10 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
                         int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                         int64_t ld, void* stream);
+// d_amp: signed amplitudes, or (kernel_values) K under the plan's convention.
 qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* d_b, int64_t n_b,
-                       const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream);
+                       const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream,
+                       bool kernel_values = false);
 qk_status launch_dfma_peak(double* out, void* stream);
 
 enum SweepMode { kModeGram = 0, kModeCross = 1, kModeJob = 2 };

@@ -1332,7 +1332,7 @@ template <int M>
 __global__ void __launch_bounds__(kDeepThreads) pairs_deep_kernel(
     const double2* __restrict__ A, int64_t n_a, const double2* __restrict__ B, int64_t n_b,
     const int64_t* __restrict__ pairs, int64_t n_pairs, double* __restrict__ amp, int n_pad,
-    int front) {
+    int front, int value) {
   extern __shared__ double V[];
   __shared__ double red[kDeepThreads];
   constexpr int PP = Deep<M>::PP, TPS = Deep<M>::IPP;
@@ -1350,7 +1350,8 @@ __global__ void __launch_bounds__(kDeepThreads) pairs_deep_kernel(
   deep_sweep<M>(V, red, A + (sp / kTile) * int64_t(n_pad) * kTile + (sp % kTile),
                 B + (sq / kTile) * int64_t(n_pad) * kTile + (sq % kTile), front, n_pad);
   if (threadIdx.x % TPS == 0 && k < n_pairs)
-    amp[k] = ok ? red[threadIdx.x] : __longlong_as_double(0x7ff8000000000000LL);
+    amp[k] = !ok ? __longlong_as_double(0x7ff8000000000000LL)
+                 : value < 0 ? red[threadIdx.x] : kernel_value(red[threadIdx.x], value);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1362,7 +1363,7 @@ __global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ 
                                                     const int64_t* __restrict__ pairs,
                                                     int64_t n_pairs, double* __restrict__ amp,
                                                     int n_pad, int nchunks, int front,
-                                                    double final_scale) {
+                                                    double final_scale, int value) {
   using St = typename BondT<LAYERS>::type;
   const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n_pairs) return;
@@ -1385,7 +1386,8 @@ __global__ void __launch_bounds__(128) pairs_kernel(const double2* __restrict__ 
     if (LAYERS >= 2 && ch + 1 < nchunks && ((ch + 1) % kRescaleChunks) == 0)
       st_rescale<LAYERS>(s);
   }
-  amp[k] = st_amp<LAYERS>(s, final_scale);
+  const double v = st_amp<LAYERS>(s, final_scale);
+  amp[k] = value < 0 ? v : kernel_value(v, value);  // value: -1 amplitude, else convention
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1749,7 +1751,7 @@ static qk_status launch_deep_t(const SweepArgs& a, int mode, bool packed, cudaSt
 template <int M>
 static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, const void* d_b,
                                    int64_t n_b, const int64_t* d_pairs, int64_t n_pairs,
-                                   double* d_amp, cudaStream_t st) {
+                                   double* d_amp, int value, cudaStream_t st) {
   auto kern = pairs_deep_kernel<M>;
   constexpr size_t smem = Deep<M>::kSmem;
   int per_sm = 0;
@@ -1757,7 +1759,7 @@ static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, 
   const int64_t grid = (n_pairs + Deep<M>::PP - 1) / Deep<M>::PP;
   kern<<<unsigned(grid), kDeepThreads, smem, st>>>(
       static_cast<const double2*>(d_a), n_a, static_cast<const double2*>(d_b), n_b, d_pairs,
-      n_pairs, d_amp, p.width_padded, p.front_pad);
+      n_pairs, d_amp, p.width_padded, p.front_pad, value);
   return cuda_status(cudaGetLastError(), "deep pairs launch");
 }
 
@@ -1903,38 +1905,40 @@ qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t
 }
 
 qk_status launch_pairs(const Plan& p, const void* d_a, int64_t n_a, const void* d_b, int64_t n_b,
-                       const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream) {
+                       const int64_t* d_pairs, int64_t n_pairs, double* d_amp, void* stream,
+                       bool kernel_values) {
+  const int value = kernel_values ? p.convention : -1;
   if (n_pairs == 0) return QK_OK;
   const unsigned grid = unsigned((n_pairs + 127) / 128);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nchunks = p.width_padded / kChunk;
   switch (p.layers) {
-    case 5: return launch_pairs_deep<4>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
-    case 6: return launch_pairs_deep<5>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
-    case 7: return launch_pairs_deep<6>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
-    case 8: return launch_pairs_deep<7>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, st);
+    case 5: return launch_pairs_deep<4>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, value, st);
+    case 6: return launch_pairs_deep<5>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, value, st);
+    case 7: return launch_pairs_deep<6>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, value, st);
+    case 8: return launch_pairs_deep<7>(p, d_a, n_a, d_b, n_b, d_pairs, n_pairs, d_amp, value, st);
     default: break;
   }
   if (p.layers == 2)
     pairs_kernel<2><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
                                           n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
-                                          p.final_scale);
+                                          p.final_scale, value);
   else if (p.layers == 3)
     pairs_kernel<3><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
                                           n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
-                                          p.final_scale);
+                                          p.final_scale, value);
   else if (p.layers == 4)
     pairs_kernel<4><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
                                           n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
-                                          p.final_scale);
+                                          p.final_scale, value);
   else
     pairs_kernel<1><<<grid, 128, 0, st>>>(static_cast<const double2*>(d_a), n_a,
                                           static_cast<const double2*>(d_b), n_b, d_pairs,
                                           n_pairs, d_amp, p.width_padded, nchunks, p.front_pad,
-                                          p.final_scale);
+                                          p.final_scale, value);
   return cuda_status(cudaGetLastError(), "pairs launch");
 }
 

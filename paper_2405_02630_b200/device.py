@@ -193,6 +193,20 @@ def pair_amplitudes(a: Planes, b: Planes, pairs: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def pair_kernel_values(a: Planes, b: Planes, pairs: torch.Tensor) -> torch.Tensor:
+    """Kernel values K(a_p, b_q) under the plan's convention for explicit (p, q) pairs, input
+    order, computed in the pair kernel's epilogue (the SPEC's shard partial)."""
+    _require(pairs, "pairs", torch.int64)
+    _on_current(a.buf, "planes")
+    _on_current(b.buf, "planes")
+    pairs = pairs.reshape(-1, 2).contiguous()
+    out = torch.empty(pairs.shape[0], dtype=torch.float64, device=a.buf.device)
+    _native.check(_native.lib().qk_pair_kernel_values(a.plan.handle, a.ptr(), a.n, b.ptr(), b.n,
+                                                      pairs.data_ptr(), pairs.shape[0],
+                                                      out.data_ptr(), _stream()))
+    return out
+
+
 def dfma_peak_flops() -> float:
     """Measured FP64 FMA issue rate of the current device (FLOP/s, FMA = 2)."""
     import ctypes

@@ -466,8 +466,7 @@ def compute_kernel_shard(features, cfg, shard: int, n_shards: int, *, test=None,
     pairs = torch.as_tensor(enumeration_pairs(n_a, n_b, symmetric, lo, hi), device="cuda")
     px = dev.gate_build(sp, dev.angles_to_device(X))
     pa = px if symmetric else dev.gate_build(sp, dev.angles_to_device(T))
-    amp = dev.pair_amplitudes(pa, px, pairs)
-    vals = amp.abs() if convention == "magnitude" else amp * amp
+    vals = dev.pair_kernel_values(pa, px, pairs)  # |amp|^2 or |amp| in the pair kernel
     bad = [b for b in (px.bad_sample(), None if symmetric else pa.bad_sample()) if b is not None]
     if bad:
         raise RebindError("feature angles must be finite")

@@ -541,3 +541,42 @@ def test_kernel_job_auto_graph_matches_eager_and_api(rng, n):
         with pytest.raises(RebindError, match=f"operand set {2 * N}: feature angles must be"):
             job.run(tr, bad_te)
         job.run(tr, te)  # the sentinels reset on the next call
+
+
+_LAYOUT_PROBE = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2405_02630_b200 import SweepPlan
+from paper_2405_02630_b200.distributed import KernelJob
+rng = np.random.default_rng(3)
+out = {{}}
+for n in (5, 16, 33, 64):
+    tr = torch.as_tensor(rng.uniform(0, 0.4, (700, n)), device="cuda")
+    te = torch.as_tensor(rng.uniform(0, 0.4, (130, n)), device="cuda")
+    K, Kx = KernelJob(SweepPlan(n, 2), 700, 130, graph_mode=False).run(tr, te)
+    out[f"K{{n}}"], out[f"Kx{{n}}"] = K.cpu().numpy(), Kx.cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_short_chain_layouts_bit_identical(tmp_path):
+    """Short chains (n_pad <= 64) run 32-row items with all 16 warps busy (RI = 1); the
+    64-row-item layout (QK_SHORT_RI1=0) and the long-chain kernel (QK_SHORT_CHAIN=0) must give
+    the same bits — every layout runs the same per-pair recurrence."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for name, env in (("ri1", {}), ("ri2", {"QK_SHORT_RI1": "0"}),
+                      ("long", {"QK_SHORT_CHAIN": "0"})):
+        path = str(tmp_path / f"{name}.npz")
+        subprocess.run([sys.executable, "-c", _LAYOUT_PROBE.format(root=root, path=path)],
+                       check=True, env={**os.environ, **env}, timeout=300)
+        with np.load(path) as z:
+            res[name] = {k: z[k] for k in z.files}
+    for k in res["ri1"]:
+        assert np.array_equal(res["ri1"][k], res["ri2"][k]), k
+        assert np.array_equal(res["ri1"][k], res["long"][k]), k
