@@ -1230,12 +1230,127 @@ __device__ __forceinline__ void deep_pair_round(double* V, double c, double s, d
   }
 }
 
+// L = 5..7 (M <= 6, one thread per column of a pair's D x D state): the state stays in
+// registers for the whole sweep.  Layout A: thread t holds column t (x[r] = V[r][t]), so the
+// F_i^T levels (on the row index) are register-local; layout B: thread t holds row t
+// (x[c] = V[t][c]) for the F_j levels.  The row and column passes of one qubit commute, so
+// even qubits run rows -> transpose -> columns -> mask and odd ones columns -> transpose ->
+// rows -> mask: ONE transpose through the pair's shared-memory slot per qubit (each element
+// written and read once: half the shared-memory traffic of two register rounds), synchronised
+// only among the pair's D threads (a warp or, at D = 64, a named barrier) instead of the CTA.
+#ifndef QK_DEEP_REG
+#define QK_DEEP_REG 1
+#endif
+template <int M>
+__device__ __forceinline__ void pair_sync() {
+  if constexpr ((1 << M) <= 32) {
+    __syncwarp();  // the pair's threads lie in one warp (and every warp runs the same loop)
+  } else {
+    const int id = 1 + int(threadIdx.x) / (1 << M);  // named barrier of the pair's 2 warps
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(1 << M) : "memory");
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void deep_levels(double (&x)[1 << M], double c, double s) {
+  constexpr int D = 1 << M;
+#pragma unroll
+  for (int k = 0; k < M; ++k)
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+      if (e & (1 << k)) continue;
+      rot_pair(x[e], x[e | (1 << k)], c, s, k == 0 ? 0 : (e >> (k - 1)) & 1);
+    }
+}
+
+template <int M, bool ROW_OWNER>  // ROW_OWNER: thread t holds row t (layout B)
+__device__ __forceinline__ void deep_mask(double (&x)[1 << M], int t, double cd, double sd) {
+  constexpr int D = 1 << M;
+  const bool mine = (t >> (M - 1)) & 1;  // top bit of this thread's row (B) / column (A)
+#pragma unroll
+  for (int e = 0; e < D; ++e) {
+    const bool other = (e >> (M - 1)) & 1;
+    const bool tb = ROW_OWNER ? mine : other, tc = ROW_OWNER ? other : mine;
+    x[e] *= tb == tc ? cd : (tb ? sd : -sd);
+  }
+}
+
+template <int M, bool TO_ROWS>  // A -> B (TO_ROWS) or B -> A through the pair's slot v
+__device__ __forceinline__ void deep_transpose(double* v, double (&x)[1 << M], int t) {
+  constexpr int D = 1 << M, RS = D + 1;
+  pair_sync<M>();  // the previous transpose's reads of v are done
+#pragma unroll
+  for (int e = 0; e < D; ++e) v[TO_ROWS ? e * RS + t : t * RS + e] = x[e];
+  pair_sync<M>();
+#pragma unroll
+  for (int e = 0; e < D; ++e) x[e] = v[TO_ROWS ? t * RS + e : e * RS + t];
+}
+
+template <int M>
+__device__ __forceinline__ void deep_sweep_reg(double* V, double* red, const double2* pi,
+                                               const double2* pj, int q_begin, int q_end) {
+  using Dp = Deep<M>;
+  constexpr int D = Dp::D;
+  const int t = threadIdx.x % D;
+  double* v = V + (threadIdx.x / D) * Dp::kSlot;
+  double x[D];
+#pragma unroll
+  for (int e = 0; e < D; ++e) x[e] = 0.0;
+  if (t == 0) x[0] = 1.0;  // V = e_00, layout A
+  int q = q_begin;
+  for (; q + 1 < q_end; q += 2) {
+    {  // even: layout A in, B out
+      const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
+      const double cd = fma(vi.y, vj.y, vi.x * vj.x), sd = fma(vi.x, vj.y, -(vi.y * vj.x));
+      deep_levels<M>(x, vi.x, vi.y);
+      deep_transpose<M, true>(v, x, t);
+      deep_levels<M>(x, vj.x, vj.y);
+      deep_mask<M, true>(x, t, cd, sd);
+    }
+    {  // odd: layout B in, A out
+      const double2 vi = __ldg(pi + int64_t(q + 1) * kTile),
+                    vj = __ldg(pj + int64_t(q + 1) * kTile);
+      const double cd = fma(vi.y, vj.y, vi.x * vj.x), sd = fma(vi.x, vj.y, -(vi.y * vj.x));
+      deep_levels<M>(x, vj.x, vj.y);
+      deep_transpose<M, false>(v, x, t);
+      deep_levels<M>(x, vi.x, vi.y);
+      deep_mask<M, false>(x, t, cd, sd);
+    }
+  }
+  if (q < q_end) {  // a last even qubit
+    const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
+    const double cd = fma(vi.y, vj.y, vi.x * vj.x), sd = fma(vi.x, vj.y, -(vi.y * vj.x));
+    deep_levels<M>(x, vi.x, vi.y);
+    deep_transpose<M, true>(v, x, t);
+    deep_levels<M>(x, vj.x, vj.y);
+    deep_mask<M, true>(x, t, cd, sd);
+  }
+  // amp = sum(V): each thread its D values in order, then the pair's D partial sums in order
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < D; ++e) acc += x[e];
+  __syncthreads();
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
+    for (int k = 0; k < D; ++k) s += red[threadIdx.x + k];
+    red[threadIdx.x] = s;  // only this thread touches its group's first entry now
+  }
+  __syncthreads();
+}
+
 // Sweeps the PP pairs whose plane columns (qubit 0) are pi / pj for this thread's slot;
 // leaves amp of slot s in red[s * IPP].  Starts and ends with a barrier.
 template <int M>
 __device__ __forceinline__ void deep_sweep(double* V, double* red, const double2* pi,
                                            const double2* pj, int q_begin, int q_end) {
   using Dp = Deep<M>;
+  if constexpr (QK_DEEP_REG && Dp::H == 0) {
+    __syncthreads();
+    deep_sweep_reg<M>(V, red, pi, pj, q_begin, q_end);
+    return;
+  }
   for (int e = threadIdx.x; e < Dp::PP * Dp::kSlot; e += kDeepThreads)
     V[e] = (e % Dp::kSlot) == 0 ? 1.0 : 0.0;
   __syncthreads();

@@ -1,6 +1,6 @@
 """Entries/s of the train Gram by feature-map depth L = 1..8 on one GPU (device-resident
 angles, CUDA events, one warm-up), with the planner's executed FP64 flops per entry -> TFLOP/s.
-Prints one JSON line per L.  usage: python tools/layers_bench.py [L ...]"""
+Prints one JSON line per L.  usage: python tools/layers_bench.py [L | L:width:samples ...]"""
 import json
 import sys
 import time
@@ -18,8 +18,9 @@ CASES = {1: (784, 8192), 2: (784, 4096), 3: (784, 1024), 4: (784, 512), 5: (784,
          6: (784, 64), 7: (128, 48), 8: (32, 40)}
 
 
-def point(L):
-    n, N = CASES[L]
+def point(L, n=None, N=None):
+    if n is None:
+        n, N = CASES[L]
     rng = np.random.default_rng(L)
     X = torch.as_tensor(rng.uniform(0, np.pi, (N, n)), device="cuda")
     plan = SweepPlan(n, L)
@@ -49,6 +50,6 @@ def point(L):
 
 
 if __name__ == "__main__":
-    Ls = [int(a) for a in sys.argv[1:]] or list(CASES)
-    for L in Ls:
-        print(json.dumps(point(L)), flush=True)
+    for a in sys.argv[1:] or [str(L) for L in CASES]:
+        f = [int(v) for v in a.split(":")]
+        print(json.dumps(point(*f)), flush=True)
