@@ -108,6 +108,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// A warp's release of a ring stage it has finished reading: acq_rel, so every warp's reads of
+// the stage happen-before the refill that the last releaser issues (which then orders the
+// async-proxy write after them with fence.proxy.async).  Returns the previous count.
+__device__ __forceinline__ int release_stage(int* counter) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+               : "=r"(old)
+               : "r"(smem_u32(counter))
+               : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -952,9 +968,10 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       __syncwarp();  // every lane's reads of this stage have completed
       if (lane == 0) {
         // the last warp to release the stage refills it with item f + kStages
-        if (atomicAdd(&released[stage], 1) == kWarps - 1) {
+        if (release_stage(&released[stage]) == kWarps - 1) {
           if (ch == 0 && k < 32) QK_TL_ANY(160 + int(k));
           released[stage] = 0;
+          fence_proxy_async_smem();  // the generic-proxy reads before the async-proxy refill
           issue(f + kStages);
         }
       }

@@ -30,7 +30,9 @@ for L, n in ((2, 40), (1, 20), (3, 6), (4, 5), (5, 4), (6, 3), (7, 3), (8, 2)):
     Kxd = dev.cross(ps, pt)
     pairs = torch.as_tensor(np.array([[0, 1], [5, Ntr - 1], [Ntr - 1, 0]]), device="cuda")
     amp = dev.pair_amplitudes(pt, pt, pairs)
+    kv = dev.pair_kernel_values(pt, pt, pairs)
     torch.cuda.synchronize()
+    assert torch.equal(kv, amp * amp)
     assert np.array_equal(Kd.cpu().numpy(), K.entries)
     assert np.array_equal(Kxd.cpu().numpy(), Kx.entries)
     print("L", L, "ok", float(amp[0]))
@@ -53,4 +55,9 @@ for n in (64, 50):
     Kg, Kxg = KernelJob(SweepPlan(n, 2), 200, 30).run(tr, te)
     Ke, Kxe = KernelJob(SweepPlan(n, 2), 200, 30, graph_mode=False).run(tr, te)
     assert torch.equal(Kg, Ke) and torch.equal(Kxg, Kxe)
+    # explicit capture (KernelJob.graph): the captured qk_job_run on the caller's tensors
+    replay, Kr, Kxr = KernelJob(SweepPlan(n, 2), 200, 30).graph(tr, te)
+    replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Kr, Ke) and torch.equal(Kxr, Kxe)
 print("sanitize smoke ok")
