@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QK_ABI_VERSION 1
+#define QK_ABI_VERSION 2
 
 typedef enum {
   QK_OK = 0,

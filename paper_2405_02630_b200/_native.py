@@ -119,7 +119,7 @@ def lib() -> ctypes.CDLL:
             raise NativeLibraryError(f"{LIB_PATH} does not export {name}") from exc
         fn.restype = restype
         fn.argtypes = argtypes
-    if handle.qk_abi_version() != 1:
+    if handle.qk_abi_version() != 2:  # QK_ABI_VERSION
         raise NativeLibraryError("libqk ABI version mismatch")
     _lib = handle
     return _lib

@@ -18,7 +18,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_native._SIGNATURES)
-    assert lib.qk_abi_version() == 1
+    assert lib.qk_abi_version() == 2
 
 
 def test_library_is_built_for_sm100a():
