@@ -478,6 +478,13 @@ int64_t choose_head(const Plan& p, int64_t n_train, int64_t n_test, double bw_by
   return 0;
 }
 
+// Cross tile order of a host-pipeline sweep: grouped super-rows (kRectTail row-major tail rows)
+// when the result drains into pinned memory; fully row-major when it drains into pageable
+// memory, whose host-side copies (~12 GB/s) must start on each tile row as it finishes to keep
+// pace with the sweep (grouped rows finish 8 at a time: config 4's pageable call measured
+// 57.1 -> 58.2 ms with them).  The order only changes which tiles share L2, not the results.
+static int64_t rect_tail_for(const void* h_out) { return is_pinned(h_out) ? -1 : INT64_MAX; }
+
 // One row-major result matrix a sweep launch fills and the copy stream drains to the host.
 struct DrainTarget {
   double* d_K;
@@ -779,7 +786,8 @@ qk_status qk_cross_kernel_host(const qk_plan* plan, const double* h_rows, int64_
   if (qk_status s = run_and_drain(w, *p, tg, 1, [&] {
         return launch_sweep(*p, kModeCross, dPr, n_rows, dPc, n_cols, 0,
                             qk_cross_tile_count(plan, n_rows, n_cols), tg[0].d_K, n_cols,
-                            QK_OUT_DENSE, w->stream, tg[0].d_prog);
+                            QK_OUT_DENSE, w->stream, tg[0].d_prog, 0, nullptr, false,
+                            rect_tail_for(h_K));
       }, &trace))
     return s;
   static const char* const names[2] = {"test", "train"};
@@ -824,6 +832,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
   // upload, the rest while the head sweeps.
   const bool pin_in = is_pinned(h_train) && (n_test == 0 || is_pinned(h_test));
   const bool pin_out = is_pinned(h_K_train) && (n_test == 0 || is_pinned(h_K_cross));
+  const int64_t tail = pin_out ? -1 : INT64_MAX;  // see rect_tail_for
   // a pageable output is drained by host copies that can only start on finished row panels,
   // which a big head delays (the head's rows finish with their strip): keep the head at the
   // pinned-upload size there and let the rest's staging stall the GPU briefly instead
@@ -871,7 +880,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
           // counter reset, so the rest sweep's counter bumps are ordered after that reset
           if (cudaError_t e = cudaEventRecord(ev[0], st)) return cuda_err(e, "cudaEventRecord");
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, 0, n_head, dKt, dKs, st,
-                                        tg[0].d_prog, tg[1].d_prog, B))
+                                        tg[0].d_prog, tg[1].d_prog, B, nullptr, false, tail))
             return s2;
           trace.point("head_end", st);
           trace.host("head_launched");
@@ -903,7 +912,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
             return fail(s2);
           trace.point("rest_sweep_start", hs);
           if (qk_status s2 = launch_job(*p, dPt, n_train, dPs, n_test, n_head, nt, dKt, dKs, hs,
-                                        tg[0].d_prog, tg[1].d_prog, B))
+                                        tg[0].d_prog, tg[1].d_prog, B, nullptr, false, tail))
             return fail(s2);
           trace.point("rest_sweep_end", hs);
           e = cudaEventRecord(ev[1], hs);
@@ -922,7 +931,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
       return s;
     if (qk_status s = run_and_drain(w, *p, tg, n_targets, [&] {
           return launch_job(*p, dPt, n_train, dPs, n_test, 0, nt, dKt, dKs, st, tg[0].d_prog,
-                            tg[1].d_prog);
+                            tg[1].d_prog, 0, nullptr, false, tail);
         }, &trace))
       return s;
   }

@@ -22,9 +22,14 @@ constexpr int kRescaleChunks = 512 / kChunk;  // L=2: rescale the bond state by 
 constexpr int kMaxLayers = 8;       // L <= 4: registers; L = 5..8: shared-memory deep sweep
 constexpr int kGroup = 8;           // tile rows per super-row of the L2-friendly tile order
 #ifndef QK_RECT_GROUP
-#define QK_RECT_GROUP 1
+#define QK_RECT_GROUP 8
 #endif
-constexpr int kRectGroup = QK_RECT_GROUP;  // tile rows per super-row of cross tile lists
+// Cross tile lists: super-rows of kRectGroup tile rows walked column by column (each train
+// column block is read from HBM once per super-row instead of once per tile row: config 4's
+// cross pass reads 0.6 instead of 4.0 GB), except the last kRectTail tile rows, which run row
+// by row so the host pipelines' final row panels drain while the sweep still runs.
+constexpr int kRectGroup = QK_RECT_GROUP;
+constexpr int kRectTail = 2;
 
 struct Plan {
   int32_t width = 0;
@@ -79,7 +84,8 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
                        unsigned int* d_progress = nullptr, int64_t head_b = 0,
-                       unsigned long long* counter = nullptr, bool pdl = false);
+                       unsigned long long* counter = nullptr, bool pdl = false,
+                       int64_t rect_tail = -1);
 qk_status launch_unpack(const Plan& p, int mode, const double* d_packed, int64_t n_rows,
                         int64_t n_cols, int64_t tile_begin, int64_t tile_end, double* d_K,
                         int64_t ld, void* stream);
@@ -97,7 +103,8 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train = nullptr,
                      unsigned int* d_prog_cross = nullptr, int64_t head_b = 0,
-                     unsigned long long* counter = nullptr, bool pdl = false);
+                     unsigned long long* counter = nullptr, bool pdl = false,
+                     int64_t rect_tail = -1);  // -1: kRectTail; pageable host drains: all rows
 // The dynamic tile schedule's claim counter for one sweep launch, zeroed on `st` (a ring slot,
 // or a stream-ordered allocation under graph capture: *owned, free it after the launch).
 // Callers that reset it (all-ones) ahead of a gate build pass it to launch_job / launch_sweep

@@ -585,9 +585,17 @@ __host__ __device__ __forceinline__ void decode_gram(int64_t g, int64_t nb, int6
 }
 
 __host__ __device__ __forceinline__ void decode_rect(int64_t g, int64_t nb_rows, int64_t nb_cols,
-                                            int64_t& bi, int64_t& bj) {
+                                            int64_t& bi, int64_t& bj,
+                                            int64_t tail = kRectTail) {
+  const int64_t grouped = nb_rows > tail ? nb_rows - tail : 0;  // rows in super-rows
+  if (g >= grouped * nb_cols) {  // the row-major tail
+    const int64_t l = g - grouped * nb_cols;
+    bi = grouped + l / nb_cols;
+    bj = l % nb_cols;
+    return;
+  }
   const int64_t r0 = (g / (kRectGroup * nb_cols)) * kRectGroup;
-  const int64_t h = nb_rows - r0 < kRectGroup ? nb_rows - r0 : kRectGroup;
+  const int64_t h = grouped - r0 < kRectGroup ? grouped - r0 : kRectGroup;
   const int64_t local = g - r0 * nb_cols;
   bj = local / h;
   bi = r0 + local % h;
@@ -766,6 +774,7 @@ struct SweepArgs {
   int64_t n_split;  // the last n_split tiles run as two row halves each (finer last wave)
   int64_t head_b;   // Gram tile order with a B-block head (decode_gram; 0: decode_upper)
   int pdl;          // host only: launch as a programmatic dependent of the preceding kernel
+  int64_t rect_tail;  // cross tile rows swept row by row at the end of the list (decode_rect)
 };
 
 // Per-tile coordinates: tile rows/cols in plane blocks and which problem of a kModeJob launch.
@@ -840,9 +849,9 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& a) {
       if (MODE == kModeGram || (MODE == kModeJob && g < a.n_first)) {
         decode_gram(g, a.nb_rows, a.head_b, bi, bj);
       } else if (MODE == kModeCross) {
-        decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+        decode_rect(g, a.nb_rows, a.nb_cols, bi, bj, a.rect_tail);
       } else {
-        decode_rect(g - a.n_first, a.nb_rows2, a.nb_cols, bi, bj);
+        decode_rect(g - a.n_first, a.nb_rows2, a.nb_cols, bi, bj, a.rect_tail);
         c.prob = 1;
       }
       c.bi = int(bi);
@@ -1122,7 +1131,7 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
     if (MODE == kModeGram) {
       decode_upper(g, a.nb_rows, bi, bj);
     } else {
-      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj, a.rect_tail);
     }
     const int il = (sub / 4) * 16 + ty, jl = (sub % 4) * 16 + tx;
     const double2* pi = a.rows + bi * int64_t(a.n_pad) * kTile + il;
@@ -1417,7 +1426,7 @@ __global__ void __launch_bounds__(kDeepThreads) sweep_deep_kernel(const SweepArg
     if (MODE == kModeGram) {
       decode_upper(g, a.nb_rows, bi, bj);
     } else {
-      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj);
+      decode_rect(g, a.nb_rows, a.nb_cols, bi, bj, a.rect_tail);
     }
     // does any pair of the group need computing?  (uniform: every thread evaluates all)
     bool any = false;
@@ -1899,13 +1908,14 @@ qk_status launch_sweep(const Plan& p, int mode, const void* d_rows, int64_t n_ro
                        const void* d_cols, int64_t n_cols, int64_t tile_begin, int64_t tile_end,
                        double* d_out, int64_t ld_out, int out_mode, void* stream,
                        unsigned int* d_progress, int64_t head_b, unsigned long long* counter,
-                       bool pdl) {
+                       bool pdl, int64_t rect_tail) {
   if (tile_end <= tile_begin) return QK_OK;
   if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
     return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
   SweepArgs a{};
   a.next_tile = counter;
   a.pdl = pdl ? 1 : 0;
+  a.rect_tail = rect_tail < 0 ? kRectTail : rect_tail;
   if (mode == kModeGram) a.head_b = head_b;
   a.progress = d_progress;
   a.rows = static_cast<const double2*>(d_rows);
@@ -1966,7 +1976,7 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
                      int64_t n_test, int64_t tile_begin, int64_t tile_end, double* d_K_train,
                      double* d_K_cross, void* stream, unsigned int* d_prog_train,
                      unsigned int* d_prog_cross, int64_t head_b, unsigned long long* counter,
-                     bool pdl) {
+                     bool pdl, int64_t rect_tail) {
   if (tile_end <= tile_begin) return QK_OK;
   if (head_b != 0 && (p.layers > 2 || head_b % kGroup != 0))
     return set_error(QK_ERR_VALUE, "Gram head order needs layers <= 2 and a multiple of 8");
@@ -1985,11 +1995,12 @@ qk_status launch_job(const Plan& p, const void* d_train, int64_t n_train, const 
     return launch_sweep(p, kModeCross, d_test, n_test, d_train, n_train,
                         std::max(tile_begin, n_gram) - n_gram, tile_end - n_gram, d_K_cross,
                         n_train, QK_OUT_DENSE, stream, d_prog_cross, 0,
-                        gram_first ? nullptr : counter, !gram_first && pdl);
+                        gram_first ? nullptr : counter, !gram_first && pdl, rect_tail);
   }
   SweepArgs a{};
   a.next_tile = counter;
   a.pdl = pdl ? 1 : 0;
+  a.rect_tail = rect_tail < 0 ? kRectTail : rect_tail;
   a.head_b = head_b;
   a.rows = static_cast<const double2*>(d_train);
   a.cols = static_cast<const double2*>(d_train);

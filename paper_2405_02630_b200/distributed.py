@@ -136,8 +136,8 @@ def _pad(n: int, edge: int) -> int:
 
 
 def tile_costs(n_train: int, n_test: int, edge: int, group: int = 8) -> np.ndarray:
-    """Relative sweep cost of every tile of the joint list (Gram in the kernel's grouped order,
-    then cross row-major; qk_sweep.cu decode_upper / decode_rect): 1, except the tiles of
+    """Relative sweep cost of every tile of the joint list (Gram then cross, both in the
+    kernel's grouped orders; qk_sweep.cu decode_upper / decode_rect): 1, except the tiles of
     tile row 0, whose front padding rows skip the sweep in whole 4-row warps (16 real rows of
     64 cost ~1/4 of a tile, measured)."""
     nb = -(-n_train // edge) if n_train else 0
@@ -153,8 +153,30 @@ def tile_costs(n_train: int, n_test: int, edge: int, group: int = 8) -> np.ndarr
         w[idx] = row0_weight(n_train)  # Gram tile row 0 lies in super-row 0
     if nbt:
         g0 = nb * (nb + 1) // 2
-        w[g0:g0 + nb] = row0_weight(n_test)  # cross tile row 0 (test block 0)
+        bi, _ = rect_tile_coords(nbt, nb)
+        w[g0 + np.flatnonzero(bi == 0)] = row0_weight(n_test)  # cross tile row 0 (test block 0)
     return w
+
+
+RECT_GROUP, RECT_TAIL = 8, 2  # qk_internal.h kRectGroup / kRectTail
+
+
+def rect_tile_coords(nb_rows: int, nb_cols: int) -> tuple[np.ndarray, np.ndarray]:
+    """(bi, bj) of every cross tile in the sweep kernel's list order (qk_sweep.cu decode_rect:
+    super-rows of RECT_GROUP tile rows walked column by column, the last RECT_TAIL rows
+    row-major)."""
+    grouped = nb_rows - RECT_TAIL if nb_rows > RECT_TAIL else 0
+    bis, bjs = [], []
+    for r0 in range(0, grouped, RECT_GROUP):
+        h = min(RECT_GROUP, grouped - r0)
+        bis.append(np.tile(np.arange(r0, r0 + h), nb_cols))
+        bjs.append(np.repeat(np.arange(nb_cols), h))
+    for r in range(grouped, nb_rows):
+        bis.append(np.full(nb_cols, r))
+        bjs.append(np.arange(nb_cols))
+    if not bis:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64)
+    return np.concatenate(bis).astype(np.int64), np.concatenate(bjs).astype(np.int64)
 
 
 def gram_tile_coords(nb: int, group: int = 8) -> tuple[np.ndarray, np.ndarray]:
@@ -187,7 +209,8 @@ def tile_entries(n_train: int, n_test: int, edge: int) -> np.ndarray:
     bi, bj = gram_tile_coords(len(rt))
     gram = np.where(bi == bj, rt[bi] * (rt[bi] - 1) // 2, rt[bi] * rt[bj])
     rs = real(n_test)
-    cross = np.outer(rs, rt).ravel()  # row-major tile list (kRectGroup = 1)
+    ci, cj = rect_tile_coords(len(rs), len(rt))
+    cross = rs[ci] * rt[cj]
     return np.concatenate([gram, cross])
 
 

@@ -3,6 +3,15 @@
 #include "qk_sweep.cu"
 #include <set>
 int main(int argc, char** argv) {
+  if (argc == 4) {  // "rect nbr nb": the cross tile list in kernel order, one "bi bj" per line
+    const int64_t nbr = atoll(argv[2]), nb = atoll(argv[3]);
+    for (int64_t g = 0; g < nbr * nb; ++g) {
+      int64_t bi, bj;
+      qk::decode_rect(g, nbr, nb, bi, bj);
+      printf("%ld %ld\n", (long)bi, (long)bj);
+    }
+    return 0;
+  }
   if (argc == 3) {  // "coords nb": the Gram tile list in kernel order, one "bi bj" per line
     const int64_t nb = atoll(argv[2]);
     for (int64_t g = 0; g < nb * (nb + 1) / 2; ++g) {

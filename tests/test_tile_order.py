@@ -33,3 +33,10 @@ def test_tile_decode_is_a_bijection(tmp_path):
         want = np.array([[int(v) for v in l.split()] for l in out.strip().splitlines()])
         bi, bj = gram_tile_coords(nb)
         assert np.array_equal(np.stack([bi, bj], 1), want), nb
+    from paper_2405_02630_b200.distributed import rect_tile_coords
+    for nbr, nb in ((1, 5), (2, 9), (3, 9), (10, 7), (11, 4), (32, 157)):
+        out = subprocess.run([str(exe), "rect", str(nbr), str(nb)], capture_output=True,
+                             text=True, check=True).stdout
+        want = np.array([[int(v) for v in l.split()] for l in out.strip().splitlines()])
+        bi, bj = rect_tile_coords(nbr, nb)
+        assert np.array_equal(np.stack([bi, bj], 1), want), (nbr, nb)

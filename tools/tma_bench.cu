@@ -5,6 +5,7 @@
 // 2 = CTAs read overlapping windows (CTA b starts at b * 16 KB mod SPAN).
 // build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/tma_bench tools/tma_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -38,7 +39,7 @@ __global__ void tma_kernel(const char* src, size_t span, int chunk, int stages, 
   cyc[blockIdx.x] = clock64() - t0;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t total = size_t(1) << 31;  // 2 GB source
@@ -53,6 +54,15 @@ int main() {
       {0, 8 << 20, 32768, 4, sms}, {1, 65536, 16384, 4, sms}, {1, 1 << 20, 16384, 4, sms},
       {2, 1 << 20, 16384, 4, sms}, {2, 8 << 20, 16384, 4, sms}, {0, 8 << 20, 16384, 4, 1},
       {1, 65536, 16384, 4, 1}};
+  if (argc > 1) {  // L2 sharing probe: every CTA streams the same SPAN once (ncu: DRAM bytes)
+    const size_t span = size_t(atoi(argv[1])) << 20;
+    const int iters = int(span / 16384);
+    const int mode = argc > 2 ? atoi(argv[2]) : 1;
+    tma_kernel<<<sms, 32, 4 * 16384 + 32>>>(src, span, 16384, 4, iters, mode, cyc);
+    cudaDeviceSynchronize();
+    printf("probe span %zu MB x %d CTAs\n", span >> 20, sms);
+    return 0;
+  }
   for (auto& c : cases) {
     const int iters = 2000;
     const size_t smem = size_t(c.stages) * c.chunk + 8 * c.stages;
