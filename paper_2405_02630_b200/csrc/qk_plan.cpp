@@ -110,11 +110,20 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   } else {
     // L >= 5, D = 2^(L-1), V is D x D (E = D^2 elements).  Per qubit per pair: two sides of
     // M = L-1 level passes, each D^2/2 rotations of 2 DMUL + 2 DFMA (6 flops); cos/sin of
-    // delta/2 (2 DMUL + 2 DFMA); the RY(delta) mask (E DMUL).  E - 1 adds and the square last.
-    const int64_t M = layers - 1, E = int64_t(1) << (2 * M);
-    in.dp_instr_per_entry = (4 * M * E + E + 4) * n + E;
-    in.flops_per_entry = (6 * M * E + E + 6) * n + E;
-    in.algorithmic_flops_per_entry = in.flops_per_entry;
+    // delta/2 (2 DMUL + 2 DFMA); the RY(delta) mask (E DMUL).  E - 1 adds and the square last
+    // (algorithmic).  Executed, L = 5..7 (qk_sweep.cu deep_sweep_reg, D threads per pair):
+    // every thread forms cos/sin of delta/2 and 4 mask-scaled level-0 coefficients per qubit
+    // (the mask is folded into the next qubit's first level), one pending mask and the sums
+    // (2 E) at the end; L = 8 (shared-memory rounds) as the algorithmic count.
+    const int64_t M = layers - 1, D = int64_t(1) << M, E = D * D;
+    in.algorithmic_flops_per_entry = (6 * M * E + E + 6) * n + E;
+    if (layers <= 7) {
+      in.dp_instr_per_entry = (4 * M * E + 8 * D) * n + 2 * E;
+      in.flops_per_entry = (6 * M * E + 10 * D) * n + 2 * E;
+    } else {
+      in.dp_instr_per_entry = (4 * M * E + E + 4) * n + E;
+      in.flops_per_entry = in.algorithmic_flops_per_entry;
+    }
     in.reference_cmacs_per_entry = 0;
   }
   *out_plan = h;

@@ -1277,28 +1277,41 @@ __device__ __forceinline__ void pair_sync() {
   }
 }
 
+// All M levels of one side on this thread's D values.  The previous qubit's RY(delta) mask is
+// folded into level 0 (a pair differing in bit 0 shares its top bit, hence its mask factor):
+// m0 / m1 scale the elements whose register top bit is 0 / 1.
 template <int M>
-__device__ __forceinline__ void deep_levels(double (&x)[1 << M], double c, double s) {
+__device__ __forceinline__ void deep_levels(double (&x)[1 << M], double c, double s, double m0,
+                                            double m1) {
   constexpr int D = 1 << M;
+  const double c0 = c * m0, s0 = s * m0, c1 = c * m1, s1 = s * m1;
 #pragma unroll
-  for (int k = 0; k < M; ++k)
+  for (int e = 0; e < D; e += 2) {
+    const bool top = (e >> (M - 1)) & 1;
+    rot_pair(x[e], x[e + 1], top ? c1 : c0, top ? s1 : s0, 0);
+  }
+#pragma unroll
+  for (int k = 1; k < M; ++k)
 #pragma unroll
     for (int e = 0; e < D; ++e) {
       if (e & (1 << k)) continue;
-      rot_pair(x[e], x[e | (1 << k)], c, s, k == 0 ? 0 : (e >> (k - 1)) & 1);
+      rot_pair(x[e], x[e | (1 << k)], c, s, (e >> (k - 1)) & 1);
     }
 }
 
-template <int M, bool ROW_OWNER>  // ROW_OWNER: thread t holds row t (layout B)
-__device__ __forceinline__ void deep_mask(double (&x)[1 << M], int t, double cd, double sd) {
-  constexpr int D = 1 << M;
-  const bool mine = (t >> (M - 1)) & 1;  // top bit of this thread's row (B) / column (A)
-#pragma unroll
-  for (int e = 0; e < D; ++e) {
-    const bool other = (e >> (M - 1)) & 1;
-    const bool tb = ROW_OWNER ? mine : other, tc = ROW_OWNER ? other : mine;
-    x[e] *= tb == tc ? cd : (tb ? sd : -sd);
-  }
+// The RY(delta) mask factors of this thread's two element groups (register top bit 0 / 1);
+// ROW_OWNER: thread t holds row t (layout B), else column t (layout A).
+template <int M, bool ROW_OWNER>
+__device__ __forceinline__ void deep_mask_factors(int t, double cd, double sd, double& m0,
+                                                  double& m1) {
+  const bool mine = (t >> (M - 1)) & 1;
+  // element top bits (tb: row, tc: column) = (mine, g) for a row owner, (g, mine) otherwise
+  auto f = [&](bool g) {
+    const bool tb = ROW_OWNER ? mine : g, tc = ROW_OWNER ? g : mine;
+    return tb == tc ? cd : (tb ? sd : -sd);
+  };
+  m0 = f(false);
+  m1 = f(true);
 }
 
 template <int M, bool TO_ROWS>  // A -> B (TO_ROWS) or B -> A through the pair's slot v
@@ -1323,34 +1336,39 @@ __device__ __forceinline__ void deep_sweep_reg(double* V, double* red, const dou
 #pragma unroll
   for (int e = 0; e < D; ++e) x[e] = 0.0;
   if (t == 0) x[0] = 1.0;  // V = e_00, layout A
+  // the mask of each qubit is deferred into the next qubit's first level (m0 / m1: pending
+  // factors of the current layout's two element groups)
+  double m0 = 1.0, m1 = 1.0;
   int q = q_begin;
   for (; q + 1 < q_end; q += 2) {
     {  // even: layout A in, B out
       const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
       const double cd = fma(vi.y, vj.y, vi.x * vj.x), sd = fma(vi.x, vj.y, -(vi.y * vj.x));
-      deep_levels<M>(x, vi.x, vi.y);
+      deep_levels<M>(x, vi.x, vi.y, m0, m1);
       deep_transpose<M, true>(v, x, t);
-      deep_levels<M>(x, vj.x, vj.y);
-      deep_mask<M, true>(x, t, cd, sd);
+      deep_levels<M>(x, vj.x, vj.y, 1.0, 1.0);
+      deep_mask_factors<M, true>(t, cd, sd, m0, m1);
     }
     {  // odd: layout B in, A out
       const double2 vi = __ldg(pi + int64_t(q + 1) * kTile),
                     vj = __ldg(pj + int64_t(q + 1) * kTile);
       const double cd = fma(vi.y, vj.y, vi.x * vj.x), sd = fma(vi.x, vj.y, -(vi.y * vj.x));
-      deep_levels<M>(x, vj.x, vj.y);
+      deep_levels<M>(x, vj.x, vj.y, m0, m1);
       deep_transpose<M, false>(v, x, t);
-      deep_levels<M>(x, vi.x, vi.y);
-      deep_mask<M, false>(x, t, cd, sd);
+      deep_levels<M>(x, vi.x, vi.y, 1.0, 1.0);
+      deep_mask_factors<M, false>(t, cd, sd, m0, m1);
     }
   }
   if (q < q_end) {  // a last even qubit
     const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
     const double cd = fma(vi.y, vj.y, vi.x * vj.x), sd = fma(vi.x, vj.y, -(vi.y * vj.x));
-    deep_levels<M>(x, vi.x, vi.y);
+    deep_levels<M>(x, vi.x, vi.y, m0, m1);
     deep_transpose<M, true>(v, x, t);
-    deep_levels<M>(x, vj.x, vj.y);
-    deep_mask<M, true>(x, t, cd, sd);
+    deep_levels<M>(x, vj.x, vj.y, 1.0, 1.0);
+    deep_mask_factors<M, true>(t, cd, sd, m0, m1);
   }
+#pragma unroll
+  for (int e = 0; e < D; ++e) x[e] *= ((e >> (M - 1)) & 1) ? m1 : m0;  // the last pending mask
   // amp = sum(V): each thread its D values in order, then the pair's D partial sums in order
   double acc = 0.0;
 #pragma unroll

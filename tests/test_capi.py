@@ -58,11 +58,16 @@ def test_plan_geometry_and_costs():
     assert q.info["width_padded"] == 32  # 15 identity qubits in front
     assert SweepPlan(5, 1).info["bond"] == 1
     assert SweepPlan(5, 3).info["bond"] == 16
-    for L in (5, 6, 7, 8):  # factored level passes: (4 M E + E + 4) n + E instructions
-        M, E = L - 1, 4 ** (L - 1)
+    for L in (5, 6, 7, 8):  # factored level passes
+        M, D = L - 1, 2 ** (L - 1)
+        E = D * D
         info = SweepPlan(5, L).info
         assert info["bond"] == E
-        assert info["dp_instr_per_entry"] == (4 * M * E + E + 4) * 5 + E
+        assert info["algorithmic_flops_per_entry"] == (6 * M * E + E + 6) * 5 + E
+        if L <= 7:  # register-resident: mask folded into level 0, per-thread coefficients
+            assert info["dp_instr_per_entry"] == (4 * M * E + 8 * D) * 5 + 2 * E
+        else:
+            assert info["dp_instr_per_entry"] == (4 * M * E + E + 4) * 5 + E
     assert SweepPlan(5, 3).info["dp_instr_per_entry"] == 112 * 5 + 9  # rotated blocked bond 16
     assert SweepPlan(5, 4).info["dp_instr_per_entry"] == 656 * 5 + 33  # rotated blocked bond 64
     assert SweepPlan(5, 4).info["bond"] == 64
