@@ -1,7 +1,8 @@
 #!/bin/bash
 # One gpurun call re-establishing the round-2 evidence: GPU tests + smoke, the bench line and
 # the reference arm, the bench's ncu launch list, full ncu captures of the config-4 sweep and
-# the gate build, and the small-job probe (BASELINE C1 / C2 / C5).
+# the gate build, the small-job probe (BASELINE C1 / C2 / C5), per-config e2e, L = 1..8
+# throughput and the pair-list kernel.
 # usage: gpurun --timeout 3000 -- 'bash tools/gpu_round_r2.sh r2e'
 TAG=${1:-r2e}
 cd "${GRAFT_REPO_ROOT:-.}"
@@ -15,6 +16,9 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
 timeout 300 python tools/gate_bench.py > gpurun_out/gate_bench_$TAG.jsonl 2>&1
 timeout 600 python tools/small_jobs.py > gpurun_out/small_jobs_$TAG.jsonl 2> gpurun_out/small_jobs_$TAG.err
+timeout 600 python tools/configs_e2e.py > gpurun_out/configs_e2e_$TAG.jsonl 2>&1
+timeout 600 python tools/layers_bench.py 1 2 3 4 5 6 7 8 5:784:512 6:784:192 7:128:256 > gpurun_out/layers_$TAG.jsonl 2>&1
+timeout 300 python tools/pairs_bench.py > gpurun_out/pairs_$TAG.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --e2e-steps 0 \
   --no-cpu-baseline > gpurun_out/launch_bench_$TAG.log 2>&1
