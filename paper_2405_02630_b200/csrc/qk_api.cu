@@ -698,12 +698,22 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
             e = cudaErrorNotSupported;
         }
         if (e != cudaSuccess) break;
+        static const char* const kReady[2][4] = {{"g0_ready", "g1_ready", "g2_ready", "g3_ready"},
+                                                 {"x0_ready", "x1_ready", "x2_ready", "x3_ready"}};
+        static const char* const kCopied[2][4] = {{"g0_copied", "g1_copied", "g2_copied",
+                                                   "g3_copied"},
+                                                  {"x0_copied", "x1_copied", "x2_copied",
+                                                   "x3_copied"}};
+        const int64_t pi = r0 / step;  // first and last panels of each target traced
+        const int ti = pi < 2 ? int(pi) : (r1 == nbr ? 3 : (r1 + step >= nbr ? 2 : -1));
+        if (trace && ti >= 0) trace->point(kReady[gram ? 0 : 1][ti], cs);
         if (!gram || t.d_prog == nullptr) {
           e = copy(row_lo(r0), row_lo(r1), 0, t.n_cols);
-          continue;
+        } else {
+          e = copy(row_lo(r0), row_lo(r1), col_lo(r0), t.n_cols);
+          if (e == cudaSuccess) e = copy(row_lo(r1), t.n_rows, col_lo(r0), col_lo(r1));
         }
-        e = copy(row_lo(r0), row_lo(r1), col_lo(r0), t.n_cols);
-        if (e == cudaSuccess) e = copy(row_lo(r1), t.n_rows, col_lo(r0), col_lo(r1));
+        if (trace && ti >= 0) trace->point(kCopied[gram ? 0 : 1][ti], cs);
       }
     }
   } else {
