@@ -716,27 +716,27 @@ __global__ void __launch_bounds__(256, MINB) gate_build_kernel(GateSet s0, GateS
   double xa[QD][4];
   GateItem ga = gate_item<QD>(s0, s1, slabs, it);
   gate_load<VEC, QD>(ga, width, front, xa);
-  if (!PERSIST) {
+  if constexpr (!PERSIST) {
     gate_store<QD>(ga, n_pad, half, xa);
-    return;
-  }
-  double xb[QD][4];
-  for (;;) {  // two items per trip so the double buffer needs no register moves
-    const int64_t nb = it + gridDim.x;
-    GateItem gb;
-    if (nb < n_items) {
-      gb = gate_item<QD>(s0, s1, slabs, nb);
-      gate_load<VEC, QD>(gb, width, front, xb);
+  } else {
+    double xb[QD][4];
+    for (;;) {  // two items per trip so the double buffer needs no register moves
+      const int64_t nb = it + gridDim.x;
+      GateItem gb;
+      if (nb < n_items) {
+        gb = gate_item<QD>(s0, s1, slabs, nb);
+        gate_load<VEC, QD>(gb, width, front, xb);
+      }
+      gate_store<QD>(ga, n_pad, half, xa);
+      if (nb >= n_items) break;
+      it = nb + gridDim.x;
+      if (it < n_items) {
+        ga = gate_item<QD>(s0, s1, slabs, it);
+        gate_load<VEC, QD>(ga, width, front, xa);
+      }
+      gate_store<QD>(gb, n_pad, half, xb);
+      if (it >= n_items) break;
     }
-    gate_store<QD>(ga, n_pad, half, xa);
-    if (nb >= n_items) break;
-    it = nb + gridDim.x;
-    if (it < n_items) {
-      ga = gate_item<QD>(s0, s1, slabs, it);
-      gate_load<VEC, QD>(ga, width, front, xa);
-    }
-    gate_store<QD>(gb, n_pad, half, xb);
-    if (it >= n_items) break;
   }
 }
 
@@ -1393,41 +1393,41 @@ __device__ __forceinline__ void deep_sweep(double* V, double* red, const double2
   if constexpr (QK_DEEP_REG && Dp::H == 0) {
     __syncthreads();
     deep_sweep_reg<M>(V, red, pi, pj, q_begin, q_end);
-    return;
-  }
-  for (int e = threadIdx.x; e < Dp::PP * Dp::kSlot; e += kDeepThreads)
-    V[e] = (e % Dp::kSlot) == 0 ? 1.0 : 0.0;
-  __syncthreads();
-  for (int q = q_begin; q < q_end; ++q) {
-    const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
-    const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
-    const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
-    deep_reg_round<M, false>(V, vi.x, vi.y, cd, sd);
+  } else {
+    for (int e = threadIdx.x; e < Dp::PP * Dp::kSlot; e += kDeepThreads)
+      V[e] = (e % Dp::kSlot) == 0 ? 1.0 : 0.0;
     __syncthreads();
-    if constexpr (Dp::H > 0) {
-      deep_pair_round<M, false>(V, vi.x, vi.y, cd, sd);
+    for (int q = q_begin; q < q_end; ++q) {
+      const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
+      const double cd = fma(vi.y, vj.y, vi.x * vj.x);   // cos((x_j - x_i)/2)
+      const double sd = fma(vi.x, vj.y, -(vi.y * vj.x));  // sin((x_j - x_i)/2)
+      deep_reg_round<M, false>(V, vi.x, vi.y, cd, sd);
       __syncthreads();
+      if constexpr (Dp::H > 0) {
+        deep_pair_round<M, false>(V, vi.x, vi.y, cd, sd);
+        __syncthreads();
+      }
+      deep_reg_round<M, true>(V, vj.x, vj.y, cd, sd);
+      __syncthreads();
+      if constexpr (Dp::H > 0) {
+        deep_pair_round<M, true>(V, vj.x, vj.y, cd, sd);
+        __syncthreads();
+      }
     }
-    deep_reg_round<M, true>(V, vj.x, vj.y, cd, sd);
+    // amp = sum(V) per slot (padding entries are zero): IPP threads per slot, fixed order
+    const int w = threadIdx.x % Dp::IPP;
+    const double* v = V + (threadIdx.x / Dp::IPP) * Dp::kSlot;
+    double acc = 0.0;
+    for (int e = w; e < Dp::kSlot; e += Dp::IPP) acc += v[e];
+    red[threadIdx.x] = acc;
     __syncthreads();
-    if constexpr (Dp::H > 0) {
-      deep_pair_round<M, true>(V, vj.x, vj.y, cd, sd);
-      __syncthreads();
+    if (w == 0) {
+      double t = 0.0;
+      for (int k = 0; k < Dp::IPP; ++k) t += red[threadIdx.x + k];
+      red[threadIdx.x] = t;  // only this thread touches its group's first entry now
     }
+    __syncthreads();
   }
-  // amp = sum(V) per slot (padding entries are zero): IPP threads per slot, fixed order
-  const int w = threadIdx.x % Dp::IPP;
-  const double* v = V + (threadIdx.x / Dp::IPP) * Dp::kSlot;
-  double acc = 0.0;
-  for (int e = w; e < Dp::kSlot; e += Dp::IPP) acc += v[e];
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  if (w == 0) {
-    double t = 0.0;
-    for (int k = 0; k < Dp::IPP; ++k) t += red[threadIdx.x + k];
-    red[threadIdx.x] = t;  // only this thread touches its group's first entry now
-  }
-  __syncthreads();
 }
 
 template <int M, int MODE, int OUT>
