@@ -1189,10 +1189,14 @@ struct Deep {
   static constexpr int D = 1 << M, E = D * D, RS = D + 1;  // padded row stride (doubles)
   static constexpr int G = M < 6 ? M : 6;    // levels per register round (2^G values/thread)
   static constexpr int H = M - G;            // remaining levels: pair rounds (M = 7: one)
-  static constexpr int IPP = D << H;         // threads per pair
-  static constexpr int PP = kDeepThreads / IPP;       // pairs per CTA: 16, 8, 4, 1
+  static constexpr bool kR = (QK_DEEP_BONDR >= 1 && M == 4) || (QK_DEEP_BONDR >= 2 && M == 5);
+  static constexpr int HB = D / 2;           // kR: blocks per side, one thread per block column
+  static constexpr int IPP = kR ? HB : D << H;  // threads per pair
+  static constexpr int PP = kDeepThreads / IPP;       // pairs per CTA: 16 (32), 8, 4, 1
   static constexpr int kGroups = kTile * kTile / PP;  // pair groups (work items) per tile
-  static constexpr int kSlot = D * RS;                // doubles per pair
+  // doubles per pair (kR: [component][block row][block column], rows padded, slots offset by
+  // 8 doubles mod 16 so the two pairs of a half-warp use disjoint banks)
+  static constexpr int kSlot = kR ? 4 * HB * (HB + 1) + 8 : D * RS;
   static constexpr size_t kSmem = size_t(PP) * kSlot * sizeof(double);
 };
 
@@ -1384,13 +1388,144 @@ __device__ __forceinline__ void deep_sweep_reg(double* V, double* red, const dou
   __syncthreads();
 }
 
+// L = 5 in the rotated blocked form of L = 3, 4 (bondr_step) over registers of HB = 8 threads
+// per pair: thread t holds block column t (layout A: x[4 r + q], the lower row levels are
+// local) or block row t (layout B: x[4 c + q], the lower column levels), the two layouts
+// alternating by qubit as in deep_sweep_reg (one transpose per qubit).  The per-block
+// L = 2-type step depends on the top-level selectors (TR, TC) = bit M-2 of the block's row and
+// column; one of them is a thread bit, so each thread forms the step's eight coefficients for
+// both values of the other (all four variants are 2-term combinations of (S, Dg) and (T, E)).
+struct BCoef {
+  double a0, b0, a1, b1, a2, b2, a3, b3;
+};
+
+__device__ __forceinline__ BCoef bondr_coef(bool tr, bool tc, double C, double D, double p1,
+                                            double q1, double p2, double q2) {
+  const double opc = 1.0 + C, cm1 = C - 1.0;
+  BCoef k;
+  if (tr == tc) {  // (0, 0) / (1, 1)
+    k.a0 = opc, k.b0 = tr ? -q1 : q1, k.a1 = cm1, k.b1 = tr ? -p2 : p2;
+    k.a2 = tr ? -p1 : p1, k.b2 = -D, k.a3 = tr ? -q2 : q2, k.b3 = D;
+  } else {  // (0, 1) / (1, 0)
+    k.a0 = tr ? D : -D, k.b0 = p1, k.a1 = tr ? D : -D, k.b1 = -q2;
+    k.a2 = -q1, k.b2 = tr ? opc : -opc, k.a3 = p2, k.b3 = tr ? -cm1 : cm1;
+  }
+  return k;
+}
+
+__device__ __forceinline__ void bondr_block(double* v, const BCoef& k) {
+  const double S = v[0], Dg = v[1], T = v[2], E = v[3];
+  v[0] = fma(k.b0, Dg, k.a0 * S);
+  v[1] = fma(k.b1, E, k.a1 * T);
+  v[2] = fma(k.b2, E, k.a2 * T);
+  v[3] = fma(k.b3, Dg, k.a3 * S);
+}
+
+template <int M>
+__device__ __forceinline__ void bondr_lower(double (&x)[4 << (M - 1)], double c, double s) {
+  constexpr int HB = 1 << (M - 1);
+#pragma unroll
+  for (int k = 0; k < M - 1; ++k)
+#pragma unroll
+    for (int b = 0; b < HB; ++b) {
+      if (b & (1 << k)) continue;
+      const int b1 = b | (1 << k), sel = k == 0 ? 0 : (b >> (k - 1)) & 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rot_pair(x[4 * b + q], x[4 * b1 + q], c, s, sel);
+    }
+}
+
+template <int M, bool TO_ROWS>  // A -> B (TO_ROWS) or B -> A through the pair's slot v
+__device__ __forceinline__ void bondr_transpose(double* v, double (&x)[4 << (M - 1)], int t) {
+  constexpr int HB = 1 << (M - 1), RS = HB + 1, QS = HB * RS;
+  __syncwarp();  // the previous transpose's reads of v are done
+#pragma unroll
+  for (int b = 0; b < HB; ++b)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q * QS + (TO_ROWS ? b * RS + t : t * RS + b)] = x[4 * b + q];
+  __syncwarp();
+#pragma unroll
+  for (int b = 0; b < HB; ++b)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[4 * b + q] = v[q * QS + (TO_ROWS ? t * RS + b : b * RS + t)];
+}
+
+template <int M>
+__device__ __forceinline__ void deep_sweep_bondr(double* V, double* red, const double2* pi,
+                                                 const double2* pj, int q_begin, int q_end,
+                                                 double final_scale) {
+  using Dp = Deep<M>;
+  constexpr int HB = Dp::HB, N = 4 * HB;
+  static_assert(HB <= 32, "a pair within one warp");
+  const int t = threadIdx.x % HB;
+  double* v = V + (threadIdx.x / HB) * Dp::kSlot;
+  const bool tbit = (t >> (M - 2)) & 1;  // this thread's block row (B) / column (A) selector
+  double x[N];
+#pragma unroll
+  for (int e = 0; e < N; ++e) x[e] = 0.0;
+  if (t == 0) x[0] = x[2] = 1.0;  // block (0, 0) as bondr_init, layout A
+  auto qubit = [&](int q, bool even) {
+    const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
+    const double ci = vi.x, si = vi.y, cj = vj.x, sj = vj.y;
+    const double ai = fma(ci, ci, -(si * si)), bi = (ci + ci) * si;
+    const double aj = fma(cj, cj, -(sj * sj)), bj = (cj + cj) * sj;
+    const double C = fma(bi, bj, ai * aj), D = fma(-bi, aj, ai * bj);
+    const double p1 = ai + aj, q1 = bi + bj, p2 = bj - bi, q2 = ai - aj;
+    if (even) {  // A: rows, transpose, B: columns, blocks (t, c): TR = tbit, TC = bit of c
+      bondr_lower<M>(x, ci, si);
+      bondr_transpose<M, true>(v, x, t);
+      bondr_lower<M>(x, cj, sj);
+      const BCoef k0 = bondr_coef(tbit, false, C, D, p1, q1, p2, q2);
+      const BCoef k1 = bondr_coef(tbit, true, C, D, p1, q1, p2, q2);
+#pragma unroll
+      for (int b = 0; b < HB; ++b) bondr_block(x + 4 * b, ((b >> (M - 2)) & 1) ? k1 : k0);
+    } else {  // B: columns, transpose, A: rows, blocks (r, t): TR = bit of r, TC = tbit
+      bondr_lower<M>(x, cj, sj);
+      bondr_transpose<M, false>(v, x, t);
+      bondr_lower<M>(x, ci, si);
+      const BCoef k0 = bondr_coef(false, tbit, C, D, p1, q1, p2, q2);
+      const BCoef k1 = bondr_coef(true, tbit, C, D, p1, q1, p2, q2);
+#pragma unroll
+      for (int b = 0; b < HB; ++b) bondr_block(x + 4 * b, ((b >> (M - 2)) & 1) ? k1 : k0);
+    }
+    if ((q + 1) % (kChunk * kRescaleChunks) == 0 && q + 1 < q_end) {  // as the L = 3, 4 sweep
+#pragma unroll
+      for (int e = 0; e < N; ++e) x[e] *= 0x1p-512;
+    }
+  };
+  int q = q_begin;
+  for (; q + 1 < q_end; q += 2) {
+    qubit(q, true);
+    qubit(q + 1, false);
+  }
+  if (q < q_end) qubit(q, true);
+  // amp = sum over blocks of (S + Dg) (bondr_amp): each thread its blocks in order, then the
+  // pair's HB partial sums in order
+  double acc = 0.0;
+#pragma unroll
+  for (int b = 0; b < HB; ++b) acc += x[4 * b] + x[4 * b + 1];
+  __syncthreads();
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double sum = 0.0;
+    for (int k = 0; k < HB; ++k) sum += red[threadIdx.x + k];
+    red[threadIdx.x] = sum * final_scale;
+  }
+  __syncthreads();
+}
+
 // Sweeps the PP pairs whose plane columns (qubit 0) are pi / pj for this thread's slot;
 // leaves amp of slot s in red[s * IPP].  Starts and ends with a barrier.
 template <int M>
 __device__ __forceinline__ void deep_sweep(double* V, double* red, const double2* pi,
-                                           const double2* pj, int q_begin, int q_end) {
+                                           const double2* pj, int q_begin, int q_end,
+                                           double final_scale) {
   using Dp = Deep<M>;
-  if constexpr (QK_DEEP_REG && Dp::H == 0) {
+  if constexpr (Dp::kR) {
+    __syncthreads();
+    deep_sweep_bondr<M>(V, red, pi, pj, q_begin, q_end, final_scale);
+  } else if constexpr (QK_DEEP_REG && Dp::H == 0) {
     __syncthreads();
     deep_sweep_reg<M>(V, red, pi, pj, q_begin, q_end);
   } else {
@@ -1458,7 +1593,8 @@ __global__ void __launch_bounds__(kDeepThreads) sweep_deep_kernel(const SweepArg
     const int pl = grp * PP + my_slot, il = pl / kTile, jl = pl % kTile;
     if (any) {
       deep_sweep<M>(V, red, a.rows + bi * int64_t(a.n_pad) * kTile + il,
-                    a.cols + bj * int64_t(a.n_pad) * kTile + jl, a.front, a.n_pad);
+                    a.cols + bj * int64_t(a.n_pad) * kTile + jl, a.front, a.n_pad,
+                    a.final_scale);
     }
     if (threadIdx.x % TPS == 0) {
       const int64_t i = bi * kTile + il - a.pad_rows, j = bj * kTile + jl - a.pad_cols;
@@ -1491,7 +1627,7 @@ template <int M>
 __global__ void __launch_bounds__(kDeepThreads) pairs_deep_kernel(
     const double2* __restrict__ A, int64_t n_a, const double2* __restrict__ B, int64_t n_b,
     const int64_t* __restrict__ pairs, int64_t n_pairs, double* __restrict__ amp, int n_pad,
-    int front, int value) {
+    int front, int value, double final_scale) {
   extern __shared__ double V[];
   __shared__ double red[kDeepThreads];
   constexpr int PP = Deep<M>::PP, TPS = Deep<M>::IPP;
@@ -1507,7 +1643,8 @@ __global__ void __launch_bounds__(kDeepThreads) pairs_deep_kernel(
   if (!ok) p = q = 0;  // sweep a valid column; the result is discarded
   const int64_t sp = p + sample_pad(n_a), sq = q + sample_pad(n_b);  // plane slots
   deep_sweep<M>(V, red, A + (sp / kTile) * int64_t(n_pad) * kTile + (sp % kTile),
-                B + (sq / kTile) * int64_t(n_pad) * kTile + (sq % kTile), front, n_pad);
+                B + (sq / kTile) * int64_t(n_pad) * kTile + (sq % kTile), front, n_pad,
+                final_scale);
   if (threadIdx.x % TPS == 0 && k < n_pairs)
     amp[k] = !ok ? __longlong_as_double(0x7ff8000000000000LL)
                  : value < 0 ? red[threadIdx.x] : kernel_value(red[threadIdx.x], value);
@@ -1918,7 +2055,7 @@ static qk_status launch_pairs_deep(const Plan& p, const void* d_a, int64_t n_a, 
   const int64_t grid = (n_pairs + Deep<M>::PP - 1) / Deep<M>::PP;
   kern<<<unsigned(grid), kDeepThreads, smem, st>>>(
       static_cast<const double2*>(d_a), n_a, static_cast<const double2*>(d_b), n_b, d_pairs,
-      n_pairs, d_amp, p.width_padded, p.front_pad, value);
+      n_pairs, d_amp, p.width_padded, p.front_pad, value, p.final_scale);
   return cuda_status(cudaGetLastError(), "deep pairs launch");
 }
 

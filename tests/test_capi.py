@@ -64,7 +64,9 @@ def test_plan_geometry_and_costs():
         info = SweepPlan(5, L).info
         assert info["bond"] == E
         assert info["algorithmic_flops_per_entry"] == (6 * M * E + E + 6) * 5 + E
-        if L <= 7:  # register-resident: mask folded into level 0, per-thread coefficients
+        if L == 5:  # rotated blocked form over D / 2 threads per pair
+            assert info["dp_instr_per_entry"] == (4 * (M - 1) * E + 2 * E + 9 * D) * 5 + E // 2 + D // 2
+        elif L <= 7:  # register-resident: mask folded into level 0, per-thread coefficients
             assert info["dp_instr_per_entry"] == (4 * M * E + 8 * D) * 5 + 2 * E
         else:
             assert info["dp_instr_per_entry"] == (4 * M * E + E + 4) * 5 + E
