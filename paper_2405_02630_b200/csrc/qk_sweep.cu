@@ -1175,13 +1175,16 @@ __global__ void __launch_bounds__(256) sweep_general_kernel(const SweepArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
-// L = 5..8 (D = 16..128, state 2 KB..128 KB per pair): the D x D state of PP pairs lives in
-// shared memory (rows padded to D + 1 doubles: conflict-free row and column walks) and a CTA
-// of 256 threads sweeps them.  Per qubit two register rounds: each thread loads one column
-// (F_i side: all M row-level passes in registers) or one row (F_j side + the RY(delta) mask),
-// so every element crosses shared memory once per side; a CTA barrier after each round.  At
-// L = 8 (D = 128) a thread holds half a column / row (64 values) and the top level is one
-// extra pair round.  Shared by the tile kernel and the pair-list kernel (bit-identical).
+// L = 5..8 (D = 16..128, state 2 KB..128 KB per pair), PP pairs per CTA of 256 threads.
+// L = 5: the rotated blocked form in registers (deep_sweep_bondr); L = 6, 7: the state in
+// registers, one thread per column / row (deep_sweep_reg); both with one shared-memory
+// transpose per qubit.  L = 8 (round 1's scheme): the D x D state in shared memory (rows
+// padded to D + 1 doubles: conflict-free row and column walks); per qubit two register
+// rounds: each thread loads one column (F_i side: all M row-level passes in registers) or one
+// row (F_j side + the RY(delta) mask), so every element crosses shared memory once per side; a
+// CTA barrier after each round; a thread holds half a column / row (64 values) and the top
+// level is one extra pair round.  Shared by the tile kernel and the pair-list kernel
+// (bit-identical).
 // ------------------------------------------------------------------------------------------
 constexpr int kDeepThreads = 256;
 template <int M>
@@ -1260,8 +1263,8 @@ __device__ __forceinline__ void deep_pair_round(double* V, double c, double s, d
   }
 }
 
-// L = 5..7 (M <= 6, one thread per column of a pair's D x D state): the state stays in
-// registers for the whole sweep.  Layout A: thread t holds column t (x[r] = V[r][t]), so the
+// L = 6, 7 (and L = 5 with QK_DEEP_BONDR=0; one thread per column of a pair's D x D state):
+// the state stays in registers for the whole sweep.  Layout A: thread t holds column t (x[r] = V[r][t]), so the
 // F_i^T levels (on the row index) are register-local; layout B: thread t holds row t
 // (x[c] = V[t][c]) for the F_j levels.  The row and column passes of one qubit commute, so
 // even qubits run rows -> transpose -> columns -> mask and odd ones columns -> transpose ->
