@@ -722,15 +722,22 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
       e = enqueue(idx, w->stage[idx & 1]);
       if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[idx & 1], cs);
     }
+    static const char* const kLanded[4] = {"p-4_landed", "p-3_landed", "p-2_landed",
+                                           "p-1_landed"};
+    static const char* const kCopied[4] = {"p-4_copied", "p-3_copied", "p-2_copied",
+                                           "p-1_copied"};
     for (size_t idx = 0; idx < np && e == cudaSuccess; ++idx) {
       const int slot = int(idx & 1);
       e = cudaEventSynchronize(w->stage_ev[slot]);
       if (e != cudaSuccess) break;
+      const int last = int(np - 1 - idx);  // trace the last four panels (host side)
+      if (trace && last < 4) trace->host(kLanded[3 - last]);
       const DrainTarget& t = tg[panels[idx].k];
       int64_t i0, i1;
       rows_of(panels[idx], i0, i1);
       copy_pool().copy(t.h_K + i0 * t.n_cols, w->stage[slot],
                        size_t(i1 - i0) * t.n_cols * sizeof(double));
+      if (trace && last < 4) trace->host(kCopied[3 - last]);
       if (idx + 2 < np) {
         e = enqueue(idx + 2, w->stage[slot]);
         if (e == cudaSuccess) e = cudaEventRecord(w->stage_ev[slot], cs);
