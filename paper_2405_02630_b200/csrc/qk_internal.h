@@ -61,20 +61,17 @@ QK_HD inline int sample_pad(int64_t n) { return int((kTile - n % kTile) % kTile)
 // of the last wave may run as two row halves, one each), L = 3, 4
 // one per 16x16 sub-tile, L >= 5 one per pair group of the deep sweep (16, 8, 4, 1 pairs at
 // L = 5, 6, 7, 8: Deep<M>::PP in qk_sweep.cu).
-// QK_DEEP_BONDR: L = 5 (1, default) or L = 5, 6 (2) in the rotated blocked form (qk_sweep.cu
-// deep_sweep_bondr: D / 2 threads per pair, twice the pairs per CTA) instead of one thread
-// per column of the state (0).  Measured (784 qubits, Gram): L = 5 3.86 -> 4.34 M entries/s;
-// L = 6 0.78 -> 0.72 M (206 registers per thread halve the resident warps), so not L = 6.
+// QK_DEEP_BONDR: L = 5 in the rotated blocked form (qk_sweep.cu deep_sweep_bondr: D / 2 threads
+// per pair, twice the pairs per CTA; 1, default) or one thread per column of the state (0).
+// Measured (784 qubits, Gram): L = 5 3.86 -> 4.34 M entries/s.  At L = 6 the blocked form
+// needs 206 registers per thread (0.72 vs 0.78 M entries/s), so L = 6 keeps the column form.
 #ifndef QK_DEEP_BONDR
 #define QK_DEEP_BONDR 1
 #endif
 QK_HD constexpr uint32_t progress_unit(int layers) {
   if (layers <= 2) return 2u;
   if (layers <= 4) return 16u;
-  const int pp = layers == 5   ? (QK_DEEP_BONDR >= 1 ? 32 : 16)
-                 : layers == 6 ? (QK_DEEP_BONDR >= 2 ? 16 : 8)
-                 : layers == 7 ? 4
-                               : 1;
+  const int pp = layers == 5 ? (QK_DEEP_BONDR ? 32 : 16) : layers == 6 ? 8 : layers == 7 ? 4 : 1;
   return uint32_t(kTile * kTile / pp);
 }
 

@@ -64,8 +64,7 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
   p.width_padded = ((width + kChunk - 1) / kChunk) * kChunk;
   p.front_pad = p.width_padded - width;
   const int nchunks = p.width_padded / kChunk;
-  if ((layers >= 2 && layers <= 4) || (QK_DEEP_BONDR >= 1 && layers == 5) ||
-      (QK_DEEP_BONDR >= 2 && layers == 6)) {
+  if ((layers >= 2 && layers <= 4) || (QK_DEEP_BONDR && layers == 5)) {
     // The rotated recurrences (bond 4, the blocked bonds 16 / 64 / 256) drop a factor 1/2 per processed
     // qubit (the identity qubits of the front padding are skipped, not processed); the kernels
     // multiply the state by 2^-512 after every kRescaleChunks chunks.
@@ -118,7 +117,7 @@ qk_status qk_plan_create(int32_t width, int32_t layers, int32_t convention, qk_p
     // (2 E) at the end; L = 8 (shared-memory rounds) as the algorithmic count.
     const int64_t M = layers - 1, D = int64_t(1) << M, E = D * D, HB = D / 2;
     in.algorithmic_flops_per_entry = (6 * M * E + E + 6) * n + E;
-    if ((QK_DEEP_BONDR >= 1 && layers == 5) || (QK_DEEP_BONDR >= 2 && layers == 6)) {
+    if (QK_DEEP_BONDR && layers == 5) {
       // rotated blocked form (deep_sweep_bondr): lower levels 4 (M-1) E, the E/4 block steps
       // 2 E, and per thread (HB per pair) 18 instructions of angles and coefficients; the sum
       in.dp_instr_per_entry = (4 * (M - 1) * E + 2 * E + 18 * HB) * n + E / 2 + HB;

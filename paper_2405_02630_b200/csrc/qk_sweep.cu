@@ -1192,8 +1192,8 @@ struct Deep {
   static constexpr int D = 1 << M, E = D * D, RS = D + 1;  // padded row stride (doubles)
   static constexpr int G = M < 6 ? M : 6;    // levels per register round (2^G values/thread)
   static constexpr int H = M - G;            // remaining levels: pair rounds (M = 7: one)
-  static constexpr bool kR = (QK_DEEP_BONDR >= 1 && M == 4) || (QK_DEEP_BONDR >= 2 && M == 5);
-  static constexpr int HB = D / 2;           // kR: blocks per side, one thread per block column
+  static constexpr bool kR = QK_DEEP_BONDR && M == 4;  // the rotated blocked form (L = 5)
+  static constexpr int HB = D / 2;           // kR: blocks per side
   static constexpr int IPP = kR ? HB : D << H;  // threads per pair
   static constexpr int PP = kDeepThreads / IPP;       // pairs per CTA: 16 (32), 8, 4, 1
   static constexpr int kGroups = kTile * kTile / PP;  // pair groups (work items) per tile
@@ -1424,13 +1424,23 @@ __device__ __forceinline__ void bondr_block(double* v, const BCoef& k) {
   v[3] = fma(k.b3, Dg, k.a3 * S);
 }
 
+// Per-pair thread geometry of the blocked form: HB block columns (layout A) / rows (B), one
+// thread each, holding the column's / row's NB = HB blocks (4 components each).  (Splitting a
+// column over two lanes for L = 6, with the top lower level as a lane exchange, measured 12 %
+// slower than the column-per-thread form: 0.69 vs 0.78 M entries/s at 784 qubits.)
 template <int M>
-__device__ __forceinline__ void bondr_lower(double (&x)[4 << (M - 1)], double c, double s) {
-  constexpr int HB = 1 << (M - 1);
+struct BondRGeo {
+  static constexpr int HB = 1 << (M - 1), NB = HB, N = 4 * NB;
+};
+
+// The lower levels (k = 0 .. M-2) on the owned block index, register-local.
+template <int M>
+__device__ __forceinline__ void bondr_lower(double (&x)[BondRGeo<M>::N], double c, double s) {
+  using G = BondRGeo<M>;
 #pragma unroll
   for (int k = 0; k < M - 1; ++k)
 #pragma unroll
-    for (int b = 0; b < HB; ++b) {
+    for (int b = 0; b < G::NB; ++b) {
       if (b & (1 << k)) continue;
       const int b1 = b | (1 << k), sel = k == 0 ? 0 : (b >> (k - 1)) & 1;
 #pragma unroll
@@ -1439,18 +1449,19 @@ __device__ __forceinline__ void bondr_lower(double (&x)[4 << (M - 1)], double c,
 }
 
 template <int M, bool TO_ROWS>  // A -> B (TO_ROWS) or B -> A through the pair's slot v
-__device__ __forceinline__ void bondr_transpose(double* v, double (&x)[4 << (M - 1)], int t) {
-  constexpr int HB = 1 << (M - 1), RS = HB + 1, QS = HB * RS;
+__device__ __forceinline__ void bondr_transpose(double* v, double (&x)[BondRGeo<M>::N], int o) {
+  using G = BondRGeo<M>;
+  constexpr int RS = G::HB + 1, QS = G::HB * RS;
   __syncwarp();  // the previous transpose's reads of v are done
 #pragma unroll
-  for (int b = 0; b < HB; ++b)
+  for (int b = 0; b < G::NB; ++b)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q * QS + (TO_ROWS ? b * RS + t : t * RS + b)] = x[4 * b + q];
+    for (int q = 0; q < 4; ++q) v[q * QS + (TO_ROWS ? b * RS + o : o * RS + b)] = x[4 * b + q];
   __syncwarp();
 #pragma unroll
-  for (int b = 0; b < HB; ++b)
+  for (int b = 0; b < G::NB; ++b)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) x[4 * b + q] = v[q * QS + (TO_ROWS ? t * RS + b : b * RS + t)];
+    for (int q = 0; q < 4; ++q) x[4 * b + q] = v[q * QS + (TO_ROWS ? o * RS + b : b * RS + o)];
 }
 
 template <int M>
@@ -1458,15 +1469,16 @@ __device__ __forceinline__ void deep_sweep_bondr(double* V, double* red, const d
                                                  const double2* pj, int q_begin, int q_end,
                                                  double final_scale) {
   using Dp = Deep<M>;
-  constexpr int HB = Dp::HB, N = 4 * HB;
-  static_assert(HB <= 32, "a pair within one warp");
-  const int t = threadIdx.x % HB;
-  double* v = V + (threadIdx.x / HB) * Dp::kSlot;
-  const bool tbit = (t >> (M - 2)) & 1;  // this thread's block row (B) / column (A) selector
+  using G = BondRGeo<M>;
+  constexpr int HB = G::HB, NB = G::NB, N = G::N, TPP = HB;
+  static_assert(TPP <= 32, "a pair within one warp");
+  const int o = threadIdx.x % TPP;  // the block column (A) / row (B) this thread owns
+  double* v = V + (threadIdx.x / TPP) * Dp::kSlot;
+  const bool obit = (o >> (M - 2)) & 1;  // selector bit of this thread's owned row (B) / col (A)
   double x[N];
 #pragma unroll
   for (int e = 0; e < N; ++e) x[e] = 0.0;
-  if (t == 0) x[0] = x[2] = 1.0;  // block (0, 0) as bondr_init, layout A
+  if (o == 0) x[0] = x[2] = 1.0;  // block (0, 0) as bondr_init, layout A
   auto qubit = [&](int q, bool even) {
     const double2 vi = __ldg(pi + int64_t(q) * kTile), vj = __ldg(pj + int64_t(q) * kTile);
     const double ci = vi.x, si = vi.y, cj = vj.x, sj = vj.y;
@@ -1474,22 +1486,24 @@ __device__ __forceinline__ void deep_sweep_bondr(double* V, double* red, const d
     const double aj = fma(cj, cj, -(sj * sj)), bj = (cj + cj) * sj;
     const double C = fma(bi, bj, ai * aj), D = fma(-bi, aj, ai * bj);
     const double p1 = ai + aj, q1 = bi + bj, p2 = bj - bi, q2 = ai - aj;
-    if (even) {  // A: rows, transpose, B: columns, blocks (t, c): TR = tbit, TC = bit of c
+    // the selector of the dimension this thread holds NB blocks of: bit M-2 of the block index
+    auto held_bit = [&](int b) { return ((b >> (M - 2)) & 1) != 0; };
+    if (even) {  // A: rows, transpose, B: columns, blocks (o, b): TR = obit
       bondr_lower<M>(x, ci, si);
-      bondr_transpose<M, true>(v, x, t);
+      bondr_transpose<M, true>(v, x, o);
       bondr_lower<M>(x, cj, sj);
-      const BCoef k0 = bondr_coef(tbit, false, C, D, p1, q1, p2, q2);
-      const BCoef k1 = bondr_coef(tbit, true, C, D, p1, q1, p2, q2);
+      const BCoef k0 = bondr_coef(obit, false, C, D, p1, q1, p2, q2);
+      const BCoef k1 = bondr_coef(obit, true, C, D, p1, q1, p2, q2);
 #pragma unroll
-      for (int b = 0; b < HB; ++b) bondr_block(x + 4 * b, ((b >> (M - 2)) & 1) ? k1 : k0);
-    } else {  // B: columns, transpose, A: rows, blocks (r, t): TR = bit of r, TC = tbit
+      for (int b = 0; b < NB; ++b) bondr_block(x + 4 * b, held_bit(b) ? k1 : k0);
+    } else {  // B: columns, transpose, A: rows, blocks (b, o): TC = obit
       bondr_lower<M>(x, cj, sj);
-      bondr_transpose<M, false>(v, x, t);
+      bondr_transpose<M, false>(v, x, o);
       bondr_lower<M>(x, ci, si);
-      const BCoef k0 = bondr_coef(false, tbit, C, D, p1, q1, p2, q2);
-      const BCoef k1 = bondr_coef(true, tbit, C, D, p1, q1, p2, q2);
+      const BCoef k0 = bondr_coef(false, obit, C, D, p1, q1, p2, q2);
+      const BCoef k1 = bondr_coef(true, obit, C, D, p1, q1, p2, q2);
 #pragma unroll
-      for (int b = 0; b < HB; ++b) bondr_block(x + 4 * b, ((b >> (M - 2)) & 1) ? k1 : k0);
+      for (int b = 0; b < NB; ++b) bondr_block(x + 4 * b, held_bit(b) ? k1 : k0);
     }
     if ((q + 1) % (kChunk * kRescaleChunks) == 0 && q + 1 < q_end) {  // as the L = 3, 4 sweep
 #pragma unroll
@@ -1503,16 +1517,16 @@ __device__ __forceinline__ void deep_sweep_bondr(double* V, double* red, const d
   }
   if (q < q_end) qubit(q, true);
   // amp = sum over blocks of (S + Dg) (bondr_amp): each thread its blocks in order, then the
-  // pair's HB partial sums in order
+  // pair's TPP partial sums in order
   double acc = 0.0;
 #pragma unroll
-  for (int b = 0; b < HB; ++b) acc += x[4 * b] + x[4 * b + 1];
+  for (int b = 0; b < NB; ++b) acc += x[4 * b] + x[4 * b + 1];
   __syncthreads();
   red[threadIdx.x] = acc;
   __syncthreads();
-  if (t == 0) {
+  if (o == 0) {
     double sum = 0.0;
-    for (int k = 0; k < HB; ++k) sum += red[threadIdx.x + k];
+    for (int k = 0; k < TPP; ++k) sum += red[threadIdx.x + k];
     red[threadIdx.x] = sum * final_scale;
   }
   __syncthreads();
