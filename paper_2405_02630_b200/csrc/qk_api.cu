@@ -1,5 +1,6 @@
 // qk_api.cu — C-ABI entry points of libqk: argument validation, launches, and the
 // host-buffer pipelines behind compute_kernel_matrix / compute_cross_kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <emmintrin.h>
 
@@ -436,6 +437,53 @@ qk_status qk_dfma_peak(double* out_flops_per_s, void* stream) {
 namespace {
 
 typedef int (*StreamWaitValue32Fn)(cudaStream_t, uintptr_t, uint32_t, unsigned int);
+typedef int (*StreamBatchMemOpFn)(cudaStream_t, unsigned int, CUstreamBatchMemOpParams*,
+                                  unsigned int);
+
+// cuStreamBatchMemOp: a drain panel's row-counter waits as ONE stream command (measured: eight
+// separate cuStreamWaitValue32 per Gram super-row cost ~15-20 us of copy-stream time per panel).
+StreamBatchMemOpFn stream_batch_mem_op() {
+  static StreamBatchMemOpFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const char* v = getenv("QK_BATCH_WAITS");  // tuning: 0 = one command per wait
+    if ((v != nullptr && v[0] == '0') ||
+        cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return StreamBatchMemOpFn(nullptr);
+    }
+    return reinterpret_cast<StreamBatchMemOpFn>(p);
+  }();
+  return fn;
+}
+
+// Waits on `cs` until counter[r] >= expect(r) for every r in [r0, r1) (GEQ); 0 on success.
+template <class Expect>
+int wait_rows(StreamWaitValue32Fn wait, cudaStream_t cs, const unsigned int* counter, int64_t r0,
+              int64_t r1, Expect expect) {
+  StreamBatchMemOpFn batch = stream_batch_mem_op();
+  if (batch != nullptr && r1 - r0 > 1) {
+    CUstreamBatchMemOpParams ops[16];
+    for (int64_t r = r0; r < r1;) {
+      const int n = int(std::min<int64_t>(16, r1 - r));
+      for (int k = 0; k < n; ++k) {
+        std::memset(&ops[k], 0, sizeof(ops[k]));
+        ops[k].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+        ops[k].waitValue.address = CUdeviceptr(reinterpret_cast<uintptr_t>(counter + r + k));
+        ops[k].waitValue.value = expect(r + k);
+        ops[k].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+      }
+      if (batch(cs, unsigned(n), ops, 0) != 0) return 1;
+      r += n;
+    }
+    return 0;
+  }
+  for (int64_t r = r0; r < r1; ++r)
+    if (wait(cs, reinterpret_cast<uintptr_t>(counter + r), expect(r), 0x0) != 0) return 1;
+  return 0;
+}
 
 StreamWaitValue32Fn stream_wait_value32() {
   static StreamWaitValue32Fn fn = [] {
@@ -643,13 +691,12 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
   auto enqueue = [&](size_t idx, void* dst) -> cudaError_t {
     const Panel& pn = panels[idx];
     const DrainTarget& t = tg[pn.k];
-    if (t.d_prog != nullptr) {
+    if (t.d_prog != nullptr) {  // every tile row of the panel is complete
       const int64_t nbr = blocks_for(t.n_rows), nbc = blocks_for(t.n_cols);
-      for (int64_t r = pn.r0; r < pn.r1; ++r) {  // every tile row of the panel is complete
-        const uint32_t expect = unit * uint32_t(t.mode == kModeGram ? nbr - r : nbc);
-        if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + r), expect, 0x0) != 0)
-          return cudaErrorNotSupported;
-      }
+      if (wait_rows(wait, cs, t.d_prog, pn.r0, pn.r1, [&](int64_t r) {
+            return unit * uint32_t(t.mode == kModeGram ? nbr - r : nbc);
+          }) != 0)
+        return cudaErrorNotSupported;
     }
     int64_t i0, i1;
     rows_of(pn, i0, i1);
@@ -691,12 +738,10 @@ qk_status run_and_drain(Workspace* w, const Plan& p, DrainTarget* tg, int n_targ
                                                                     row_bytes);
       for (int64_t r0 = 0; r0 < nbr && e == cudaSuccess; r0 += step) {
         const int64_t r1 = std::min(r0 + step, nbr);
-        for (int64_t q = r0; q < r1 && t.d_prog != nullptr && e == cudaSuccess; ++q) {
-          const uint32_t expect =
-              unit * uint32_t(gram ? nbr - q : blocks_for(t.n_cols));
-          if (wait(cs, reinterpret_cast<uintptr_t>(t.d_prog + q), expect, 0x0) != 0)
-            e = cudaErrorNotSupported;
-        }
+        if (t.d_prog != nullptr && wait_rows(wait, cs, t.d_prog, r0, r1, [&](int64_t q) {
+              return unit * uint32_t(gram ? nbr - q : blocks_for(t.n_cols));
+            }) != 0)
+          e = cudaErrorNotSupported;
         if (e != cudaSuccess) break;
         static const char* const kReady[2][4] = {{"g0_ready", "g1_ready", "g2_ready", "g3_ready"},
                                                  {"x0_ready", "x1_ready", "x2_ready", "x3_ready"}};
