@@ -2,7 +2,7 @@
 run, so both ranks share cuda:0 (CUDA IPC between processes works within a device) and the
 process group is gloo; on an 8-GPU box the same code runs one rank per GPU over NCCL with
 the IPC stores going over NVLink.  Both placements must reproduce the single-process
-matrices bit for bit."""
+matrices bit for bit and, for L <= 3, the CPU oracle's to 1e-12."""
 import os
 import socket
 
@@ -55,6 +55,11 @@ def worker(rank, world, port, placement, layers, q):
             Kxr = compute_cross_kernel(Xte, Xtr, cfg).entries
             ok = (np.array_equal(K.cpu().numpy(), Kr) and np.array_equal(out_K.array, Kr),
                   np.array_equal(Kx.cpu().numpy(), Kxr) and np.array_equal(out_Kx.array, Kxr))
+            if layers <= 3:  # and the multi-rank result against the CPU oracle itself
+                from oracle import oracle
+                err = max(float(np.abs(out_K.array - oracle.kernel_matrix(Xtr, layers)).max()),
+                          float(np.abs(out_Kx.array - oracle.cross_kernel(Xte, Xtr, layers)).max()))
+                ok = (ok[0] and err <= 1e-12, ok[1] and err <= 1e-12)
             q.put(ok)
         dist.barrier()
         out_K.close()
