@@ -18,6 +18,8 @@ stay on the device.  There is no CPU compute path.
 """
 from __future__ import annotations
 
+import atexit
+import ctypes
 import mmap
 from dataclasses import dataclass, field
 from math import ceil, prod
@@ -165,13 +167,22 @@ class _HostCache:
     critical path.  Mappings of dropped results are kept here (up to ``QK_HOST_CACHE_MB``,
     default 4096; 0 disables) and handed to the next result of the same size, already faulted
     in.  A result's numpy array holds its mapping through :class:`_Mapping`, whose finaliser
-    runs only once every view of the array is gone."""
+    runs only once every view of the array is gone.
+
+    New mappings are also page-locked once (``qk_host_register``, ``QK_PIN_RESULTS=0``
+    disables): the host pipelines then drain the results straight into them per 64-row tile
+    row, as for caller-pinned buffers, instead of through the pinned staging pair and the copy
+    pool (whose last panels trail the sweep by ~1 ms at config 4).  The registration cost is
+    paid when the mapping is created and amortised by the recycling; a mapping is unregistered
+    before it is unmapped.  Without a usable CUDA device the mapping simply stays pageable."""
 
     def __init__(self):
         import os
         import threading
 
         self.limit = int(os.environ.get("QK_HOST_CACHE_MB", "4096")) << 20
+        self.pin = os.environ.get("QK_PIN_RESULTS", "1") != "0"
+        self.pinned: dict[int, int] = {}  # id(mapping) -> registered address
         self.free: dict[int, list] = {}
         self.bytes = 0
         self.lock = threading.Lock()
@@ -187,7 +198,36 @@ class _HostCache:
             buf.madvise(mmap.MADV_HUGEPAGE)
         except (AttributeError, OSError):  # pragma: no cover - platform without THP advice
             pass
+        if self.pin:
+            self._register(buf)
         return buf
+
+    def _register(self, buf) -> None:
+        try:
+            lib = _native.lib()
+            _native.bind_current_device()
+            c = ctypes.c_char.from_buffer(buf)
+            addr = ctypes.addressof(c)
+            del c  # release the export (the mapping must stay closable)
+            if lib.qk_host_register(ctypes.c_void_p(addr), ctypes.c_size_t(len(buf))) == 0:
+                self.pinned[id(buf)] = addr
+        except Exception:  # pragma: no cover - no CUDA device: a pageable result is correct
+            pass
+
+    def _release(self, buf) -> None:
+        addr = self.pinned.pop(id(buf), None)
+        if addr is not None and _native.lib().qk_host_unregister(ctypes.c_void_p(addr)) != 0:
+            return  # still registered: leave it mapped rather than unmap locked pages
+        buf.close()
+
+    def drop_all(self) -> None:
+        """Unregister and unmap every cached mapping (atexit, before CUDA tears down)."""
+        with self.lock:
+            bufs = [b for lst in self.free.values() for b in lst]
+            self.free.clear()
+            self.bytes = 0
+        for b in bufs:
+            self._release(b)
 
     def put(self, buf) -> None:
         n = len(buf)
@@ -196,10 +236,11 @@ class _HostCache:
                 self.free.setdefault(n, []).append(buf)
                 self.bytes += n
                 return
-        buf.close()
+        self._release(buf)
 
 
 _host_cache = _HostCache()
+atexit.register(_host_cache.drop_all)
 
 
 class _Mapping:

@@ -177,6 +177,29 @@ def test_pinned_output_pipeline_matches_pageable(rng):
                           compute_cross_kernel(T, X, cfg).entries)
 
 
+def test_library_results_are_page_locked_and_match_pageable_outputs(rng):
+    """Results of >= 64 MB that the API allocates live in recycled page-locked mappings
+    (kernel_pipeline._HostCache): the pipeline drains straight into them.  They must equal the
+    drain into caller-supplied pageable arrays bit for bit, across recycled calls."""
+    from paper_2405_02630_b200 import compute_kernel_matrices
+    from paper_2405_02630_b200.kernel_pipeline import _host_cache
+
+    n, N, M = 48, 3100, 2900  # 77 MB Gram, 72 MB cross
+    X = rng.uniform(0, np.pi, n) + rng.normal(0, 0.3 / np.sqrt(n), (N, n))
+    T = rng.uniform(0, np.pi, n) + rng.normal(0, 0.3 / np.sqrt(n), (M, n))
+    cfg = FeatureMapConfig(n)
+    ref_K, ref_Kx = np.zeros((N, N)), np.zeros((M, N))
+    compute_kernel_matrices(X, T, cfg, out_train=ref_K, out_test=ref_Kx)
+    for _ in range(3):  # the second and third calls get the first call's mappings back
+        K, Kx = compute_kernel_matrices(X, T, cfg)
+        registered = set(_host_cache.pinned.values())  # start addresses of the mappings
+        assert K.entries.ctypes.data in registered and Kx.entries.ctypes.data in registered
+        assert np.array_equal(K.entries, ref_K) and np.array_equal(Kx.entries, ref_Kx)
+        del K, Kx
+    i = rng.integers(0, N, 16)
+    assert np.abs(ref_K[np.ix_(i, i)] - oracle.kernel_matrix(X[i], 2)).max() <= K_ABS
+
+
 def test_full_size_gram_properties_and_sampled_parity():
     """BASELINE configs[3] at full size (10000 train Gram + 2000 x 10000 cross at 784 qubits,
     bandwidth-scaled overlapping MNIST-shaped data): size-independent properties plus 256
@@ -457,7 +480,9 @@ def test_pinned_head_first_pipeline_matches_pageable(n, n_train, n_test, rng):
                                       out_test=pinned(np.zeros((n_test, n_train))))
     assert np.array_equal(K.entries, Kp.entries)
     assert np.array_equal(Kx.entries, Kxp.entries)
-    Kq, Kxq = compute_kernel_matrices(pinned(X), pinned(T), cfg)  # pageable outputs
+    Kq, Kxq = compute_kernel_matrices(pinned(X), pinned(T), cfg,  # pageable outputs
+                                      out_train=np.zeros((n_train, n_train)),
+                                      out_test=np.zeros((n_test, n_train)))
     assert np.array_equal(K.entries, Kq.entries) and np.array_equal(Kx.entries, Kxq.entries)
     Kg = compute_kernel_matrix(pinned(X), cfg)  # Gram-only entry: the joint pipeline
     assert np.array_equal(K.entries, Kg.entries)
