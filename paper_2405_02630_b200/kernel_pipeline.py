@@ -21,6 +21,7 @@ from __future__ import annotations
 import atexit
 import ctypes
 import mmap
+import os
 from dataclasses import dataclass, field
 from math import ceil, prod
 from typing import Any, Iterable
@@ -162,7 +163,8 @@ def _is_cuda_tensor(x) -> bool:
 class _HostCache:
     """Recycles the large anonymous mappings behind result matrices.
 
-    A fresh 960 MB result (config 4) costs page faults on first touch (taken by the copy-out
+    Results of at least ``QK_MAPPED_MIN_MB`` (default 1 MB) use it.  A fresh 960 MB result
+    (config 4) costs page faults on first touch (taken by the copy-out
     pool while the sweep runs) and ~2 ms of munmap when the caller drops it — on the caller's
     critical path.  Mappings of dropped results are kept here (up to ``QK_HOST_CACHE_MB``,
     default 4096; 0 disables) and handed to the next result of the same size, already faulted
@@ -177,7 +179,6 @@ class _HostCache:
     before it is unmapped.  Without a usable CUDA device the mapping simply stays pageable."""
 
     def __init__(self):
-        import os
         import threading
 
         self.limit = int(os.environ.get("QK_HOST_CACHE_MB", "4096")) << 20
@@ -240,6 +241,10 @@ class _HostCache:
 
 
 _host_cache = _HostCache()
+# results from this size up come from the cache (QK_MAPPED_MIN_MB, default 1): page-locked,
+# they drain per tile row (config 2's default call measured 1.19 -> 0.42 ms, config 3's 4.31
+# -> 3.81 ms against the staged drain into np.empty results; profiles/r2/configs_e2e_r2l.jsonl)
+_MAPPED_MIN = int(float(os.environ.get("QK_MAPPED_MIN_MB", "1")) * (1 << 20))
 atexit.register(_host_cache.drop_all)
 
 
@@ -269,7 +274,7 @@ def host_empty(shape) -> np.ndarray:
     transparent huge pages (the first touch by the copy-out pool faults 2 MB at a time),
     recycled through :class:`_HostCache` once the caller drops them."""
     nbytes = prod(shape) * 8
-    if nbytes < (64 << 20):
+    if nbytes < _MAPPED_MIN:
         return np.empty(shape, dtype=np.float64)
     return np.frombuffer(_Mapping(_host_cache.get(nbytes)), dtype=np.float64).reshape(shape)
 

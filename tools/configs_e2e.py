@@ -1,6 +1,7 @@
 """Device-resident vs end-to-end (pinned host arrays in and out) rate for each BASELINE config
 on one GPU: KernelJob.run on resident angles (CUDA events) against compute_kernel_matrices
-host→host (wall clock), best of `reps`.  One JSON line per config."""
+host→host (wall clock), best of `reps`; and the default call (pageable numpy angles in,
+library-allocated results out: `default_ms`).  One JSON line per config."""
 import json
 import sys
 import time
@@ -32,7 +33,8 @@ for cid, n, ntr, nte in CONFIGS:
     job = KernelJob(plan_for(cfg), ntr, nte)
     tr, te = torch.as_tensor(X, device="cuda"), torch.as_tensor(T, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dev_ms, e2e_ms = [], []
+    Xp, Tp = np.array(X), np.array(T)  # pageable copies for the default call
+    dev_ms, e2e_ms, def_ms = [], [], []
     for _ in range(reps + 2):
         e0.record()
         job.run(tr, te)
@@ -42,9 +44,12 @@ for cid, n, ntr, nte in CONFIGS:
         t = time.perf_counter()
         compute_kernel_matrices(X, T, cfg, out_train=K, out_test=Kx)
         e2e_ms.append((time.perf_counter() - t) * 1e3)
-    d, e = min(dev_ms[2:]), min(e2e_ms[2:])
+        t = time.perf_counter()
+        compute_kernel_matrices(Xp, Tp, cfg)
+        def_ms.append((time.perf_counter() - t) * 1e3)
+    d, e, f = min(dev_ms[2:]), min(e2e_ms[2:]), min(def_ms[2:])
     print(json.dumps({"config": cid, "qubits": n, "n_train": ntr, "n_test": nte,
-                      "entries": entries, "device_ms": d, "e2e_ms": e,
+                      "entries": entries, "device_ms": d, "e2e_ms": e, "default_ms": f,
                       "device_entries_per_s": entries / d * 1e3,
                       "e2e_entries_per_s": entries / e * 1e3, "e2e_over_device": d / e}),
           flush=True)
