@@ -113,3 +113,39 @@ def test_host_result_mappings_are_recycled_only_after_every_view_is_gone():
     small = host_empty((10, 10))  # small results are plain numpy arrays
     assert small.base is None or not hasattr(small.base, "__buffer__")
     del b, c
+
+
+def test_result_mappings_page_locked_once_and_unlocked_before_unmap(monkeypatch):
+    """Host logic of the page-locked result cache (no GPU: libqk's register entry points are
+    replaced by counters): a mapping is registered once when created, handed back registered
+    when recycled, and unregistered before it is unmapped (cache overflow, drop_all)."""
+    from paper_2405_02630_b200 import kernel_pipeline as kp
+
+    calls = []
+
+    class FakeLib:
+        def qk_host_register(self, ptr, n):
+            calls.append(("reg", ptr.value, n.value))
+            return 0
+
+        def qk_host_unregister(self, ptr):
+            calls.append(("unreg", ptr.value))
+            return 0
+
+    monkeypatch.setattr(kp._native, "lib", lambda: FakeLib())
+    monkeypatch.setattr(kp._native, "bind_current_device", lambda: None)
+    cache = kp._HostCache()
+    cache.pin, cache.limit = True, 3 << 20
+    a = cache.get(2 << 20)
+    assert len(calls) == 1 and calls[0][0] == "reg" and calls[0][2] == 2 << 20
+    addr = calls[0][1]
+    assert cache.pinned == {id(a): addr}
+    cache.put(a)  # fits the 3 MB limit: kept, still registered
+    assert cache.get(2 << 20) is a and len(calls) == 1
+    b = cache.get(2 << 20)  # a new mapping: registered
+    assert len(calls) == 2 and calls[1][0] == "reg"
+    cache.put(a)
+    cache.put(b)  # over the limit: unregistered, then unmapped
+    assert calls[2] == ("unreg", calls[1][1]) and b.closed and id(b) not in cache.pinned
+    cache.drop_all()  # the cached one too
+    assert calls[3] == ("unreg", addr) and a.closed and cache.pinned == {} and cache.bytes == 0
