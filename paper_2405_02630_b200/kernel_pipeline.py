@@ -204,16 +204,15 @@ class _HostCache:
         return buf
 
     def _register(self, buf) -> None:
-        try:
-            lib = _native.lib()
-            _native.bind_current_device()
-            c = ctypes.c_char.from_buffer(buf)
-            addr = ctypes.addressof(c)
-            del c  # release the export (the mapping must stay closable)
-            if lib.qk_host_register(ctypes.c_void_p(addr), ctypes.c_size_t(len(buf))) == 0:
-                self.pinned[id(buf)] = addr
-        except Exception:  # pragma: no cover - no CUDA device: a pageable result is correct
-            pass
+        # a failed registration (no CUDA device, locked-memory limit) leaves a pageable result,
+        # which the pipelines drain correctly through the staging pair
+        lib = _native.lib()  # NativeLibraryError propagates: there is no engine without it
+        _native.bind_current_device()
+        c = ctypes.c_char.from_buffer(buf)
+        addr = ctypes.addressof(c)
+        del c  # release the export (the mapping must stay closable)
+        if lib.qk_host_register(ctypes.c_void_p(addr), ctypes.c_size_t(len(buf))) == 0:
+            self.pinned[id(buf)] = addr
 
     def _release(self, buf) -> None:
         addr = self.pinned.pop(id(buf), None)
