@@ -1,5 +1,5 @@
 """Randomised stress of the host pipelines (head-first two-stream overlap, per-tile-row
-drains, pinned / pageable inputs and outputs) against the
+drains, pinned / pageable inputs, pinned / library-allocated / pageable outputs) against the
 device-resident path, bit for bit.  usage: python tools/stress_pipelines.py [seconds]"""
 import os
 import sys
@@ -33,12 +33,15 @@ while time.time() - t0 < budget:
     Kd, Kxd = compute_kernel_matrices(torch.as_tensor(X, device="cuda"),
                                       torch.as_tensor(T, device="cuda"), cfg)
     Kd, Kxd = Kd.entries.cpu().numpy(), Kxd.entries.cpu().numpy()
-    pin_in, pin_out = bool(rng.integers(2)), bool(rng.integers(2))
+    # outputs: caller-pinned, library-allocated (recycled page-locked mappings from 1 MB up,
+    # holding an earlier result's values), or caller-pageable (the staged drain)
+    pin_in, pin_out = bool(rng.integers(2)), str(rng.choice(["pinned", "library", "pageable"]))
     Xi, Ti = (pin(X), pin(T)) if pin_in else (X, T)
     kw = {}
-    if pin_out:
-        kw = {"out_train": pin(np.full((ntr, ntr), np.nan)),
-              "out_test": pin(np.full((nte, ntr), np.nan))}
+    if pin_out != "library":
+        wrap = pin if pin_out == "pinned" else (lambda a: a)
+        kw = {"out_train": wrap(np.full((ntr, ntr), np.nan)),
+              "out_test": wrap(np.full((nte, ntr), np.nan))}
     K, Kx = compute_kernel_matrices(Xi, Ti, cfg, **kw)
     ok = np.array_equal(K.entries, Kd) and np.array_equal(Kx.entries, Kxd)
     cases += 1
