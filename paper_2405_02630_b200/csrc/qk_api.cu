@@ -954,7 +954,7 @@ qk_status qk_kernel_matrices_host(const qk_plan* plan, const double* h_train, in
             size_t bytes;
           } segs[2] = {{dXt + s1 * p->width, h_train + s1 * p->width, size_t(n_train - s1) * row},
                        {dXs, h_test, n_test > 0 ? xsb : 0}};
-          const size_t chunk = staged ? (size_t(16) << 20) / row * row : SIZE_MAX;
+          const size_t chunk = staged ? std::max(row, (size_t(16) << 20) / row * row) : SIZE_MAX;
           if (staged) cudaStreamQuery(st);  // flush the head launch to the device first
           cudaError_t e = cudaSuccess;
           char* stage_at = staged ? static_cast<char*>(w->in_stage) + size_t(s1) * row : nullptr;
